@@ -1,0 +1,189 @@
+"""ORACLE — test infrastructure only.
+
+ctypes binding over ``oracle/oracle.c`` (plain single-threaded C; see its
+header for what each function follows in arXiv 2411.01919).  Only ``tests/``,
+``__graft_entry__.smoke()`` and ``bench.py`` (its ``cpu_baseline`` leg and
+``--impl reference``) may import this package.  The product path
+(``paper_2411_01919_b200``) never imports it and shares no code with it.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+import threading
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "oracle.c")
+_LIB_PATH = os.path.join(_HERE, "liboracle.so")
+_lock = threading.Lock()
+_lib = None
+
+CFLAGS = ["-O2", "-std=c11", "-fPIC", "-shared", "-ffp-contract=off", "-fno-fast-math",
+          "-fvisibility=hidden", "-Wall", "-Wextra", "-Wno-unused-parameter"]
+
+SAMPLER_PHILOX, SAMPLER_ENUMERATE = 0, 1
+SELECT_COUNT, SELECT_ERROR = 0, 1
+STATUS_OK, STATUS_REJECTED, STATUS_TOO_FEW, STATUS_DEGENERATE = 0, 1, 2, 3
+
+
+def build(force: bool = False) -> str:
+    """Compile liboracle.so with gcc (no FMA contraction)."""
+    if force or not os.path.exists(_LIB_PATH) or os.path.getmtime(_LIB_PATH) < os.path.getmtime(_SRC):
+        tmp = _LIB_PATH + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", *CFLAGS, "-o", tmp, _SRC, "-lm"])
+        os.replace(tmp, _LIB_PATH)
+    return _LIB_PATH
+
+
+def lib() -> ctypes.CDLL:
+    global _lib
+    with _lock:
+        if _lib is None:
+            build()
+            L = ctypes.CDLL(_LIB_PATH)
+            P = ctypes.c_void_p
+            i32, u32, u64, f32, f64 = (ctypes.c_int, ctypes.c_uint32, ctypes.c_uint64,
+                                       ctypes.c_float, ctypes.c_double)
+            L.orc_adf.argtypes = [P, P, i32, i32, f64, f64, i32]
+            L.orc_normals.argtypes = [P, i32, i32, f64, f64, f64, f64, P]
+            L.orc_normals_f64.argtypes = [P, i32, i32, f64, f64, f64, f64, P]
+            L.orc_sobel_f64.argtypes = [P, i32, i32, P]
+            L.orc_philox4x32_10.argtypes = [P, P, P]
+            L.orc_philox4x32_10.restype = None
+            L.orc_sample_triple.argtypes = [u32, u32, u32, u32, P]
+            L.orc_sample_triple.restype = None
+            L.orc_colex_unrank3.argtypes = [u64, u32, P]
+            L.orc_deproject.argtypes = [i32, i32, f32, f32, f32, f32, f32, P]
+            L.orc_deproject.restype = None
+            L.orc_plane_from_3pts.argtypes = [P, P, P, P]
+            L.orc_point_plane_dist.argtypes = [P, P]
+            L.orc_point_plane_dist.restype = f32
+            L.orc_refit_plane.argtypes = [P, i32, P]
+            L.orc_ransac.argtypes = [P, P, i32, i32, f32, f32, f32, f32, i32, i32, f32, u64, u32,
+                                     i32, i32, P, P, P, P, P]
+            _lib = L
+    return _lib
+
+
+def _p(a: np.ndarray) -> int:
+    return a.ctypes.data
+
+
+def _c(a, dtype) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=dtype)
+
+
+def adf(depth: np.ndarray, lam: float, kappa: float, iters: int) -> np.ndarray:
+    """Alg. 1 ℓ1-8 on one f32 [H, W] frame (metres) -> f32 [H, W]."""
+    d = _c(depth, np.float32)
+    H, W = d.shape
+    out = np.empty_like(d)
+    rc = lib().orc_adf(_p(d), _p(out), W, H, float(lam), float(kappa), int(iters))
+    assert rc == 0
+    return out
+
+
+def normals(depth: np.ndarray, K) -> np.ndarray:
+    """Alg. 1 ℓ9-13 on f32 depth -> float64 [3, H, W]; (0,0,0) = invalid."""
+    d = _c(depth, np.float32)
+    H, W = d.shape
+    out = np.empty((3, H, W), np.float64)
+    rc = lib().orc_normals(_p(d), W, H, K.fx, K.fy, K.cx, K.cy, _p(out))
+    assert rc == 0
+    return out
+
+
+def normals_f64(depth: np.ndarray, K) -> np.ndarray:
+    d = _c(depth, np.float64)
+    H, W = d.shape
+    out = np.empty((3, H, W), np.float64)
+    rc = lib().orc_normals_f64(_p(d), W, H, K.fx, K.fy, K.cx, K.cy, _p(out))
+    assert rc == 0
+    return out
+
+
+def sobel_f64(depth: np.ndarray) -> np.ndarray:
+    d = _c(depth, np.float64)
+    H, W = d.shape
+    out = np.empty((2, H, W), np.float64)
+    assert lib().orc_sobel_f64(_p(d), W, H, _p(out)) == 0
+    return out
+
+
+def philox4x32_10(ctr, key) -> np.ndarray:
+    c = _c(ctr, np.uint32)
+    k = _c(key, np.uint32)
+    out = np.empty(4, np.uint32)
+    lib().orc_philox4x32_10(_p(c), _p(k), _p(out))
+    return out
+
+
+def sample_triple(r0: int, r1: int, r2: int, n: int) -> tuple:
+    out = np.empty(3, np.uint32)
+    lib().orc_sample_triple(r0, r1, r2, n, _p(out))
+    return tuple(int(x) for x in out)
+
+
+def colex_unrank3(h: int, n: int):
+    out = np.empty(3, np.uint32)
+    ok = lib().orc_colex_unrank3(h, n, _p(out))
+    return tuple(int(x) for x in out) if ok else None
+
+
+def deproject(u: int, v: int, z: float, K) -> np.ndarray:
+    out = np.empty(3, np.float32)
+    lib().orc_deproject(u, v, z, K.fx, K.fy, K.cx, K.cy, _p(out))
+    return out
+
+
+def plane_from_3pts(p0, p1, p2):
+    a, b, c = (_c(p, np.float32) for p in (p0, p1, p2))
+    out = np.zeros(4, np.float32)
+    ok = lib().orc_plane_from_3pts(_p(a), _p(b), _p(c), _p(out))
+    return (out if ok else None)
+
+
+def point_plane_dist(plane, P) -> float:
+    pl = _c(plane, np.float32)
+    q = _c(P, np.float32)
+    return float(lib().orc_point_plane_dist(_p(pl), _p(q)))
+
+
+def refit_plane(pts: np.ndarray):
+    q = _c(pts, np.float64).reshape(-1, 3)
+    out = np.zeros(7, np.float64)
+    ok = lib().orc_refit_plane(_p(q), q.shape[0], _p(out))
+    return out if ok else None
+
+
+def ransac(depth: np.ndarray, labels: np.ndarray, K, n_regions: int, n_hyp: int, tau: float,
+           seed: int, frame_id: int = 0, sampler: int = SAMPLER_PHILOX,
+           select: int = SELECT_COUNT, debug: bool = False) -> dict:
+    """Alg. 2 over every region of one frame.  Returns numpy arrays:
+    n [R,3], d [R], centroid [R,3] (float64), inliers, n_points, best_hyp,
+    status [R] (int32), errq [R] (uint64) and, with debug=True, the
+    per-hypothesis counts [R, H] (int32, -1 = invalid) and errq_all [R, H]."""
+    d = _c(depth, np.float32)
+    lab = _c(labels, np.int32)
+    H, W = d.shape
+    assert lab.shape == (H, W)
+    R = int(n_regions)
+    of = np.zeros((max(R, 1), 7), np.float64)
+    oi = np.zeros((max(R, 1), 4), np.int32)
+    oe = np.zeros(max(R, 1), np.uint64)
+    cnt = np.zeros((max(R, 1), n_hyp), np.int32) if debug else None
+    ea = np.zeros((max(R, 1), n_hyp), np.uint64) if debug else None
+    rc = lib().orc_ransac(_p(d), _p(lab), W, H, K.fx, K.fy, K.cx, K.cy, R, int(n_hyp), float(tau),
+                          int(seed) & (2**64 - 1), int(frame_id), int(sampler), int(select),
+                          _p(of), _p(oi), _p(oe),
+                          _p(cnt) if debug else None, _p(ea) if debug else None)
+    assert rc == 0
+    res = dict(n=of[:R, 0:3], d=of[:R, 3], centroid=of[:R, 4:7], inliers=oi[:R, 0],
+               n_points=oi[:R, 1], best_hyp=oi[:R, 2], status=oi[:R, 3], errq=oe[:R])
+    if debug:
+        res["counts"] = cnt[:R]
+        res["errq_all"] = ea[:R]
+    return res

@@ -1,0 +1,406 @@
+"""Pins for the oracle's Algorithm 2 (RANSAC plane fitting), and the
+helpers it is built from.  Each check is against something other than the
+oracle: worked examples (tests/golden), published known-answer vectors,
+brute force, closed forms, a library eigensolver, statistics.  No GPU."""
+import itertools
+import math
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import scenegen
+
+TAU = 0.01
+
+
+def _golden(golden_dir, name, tag):
+    with open(os.path.join(golden_dir, name)) as f:
+        return [ln.split() for ln in f if ln.strip() and not ln.startswith("#") and (tag is None or ln.startswith(tag + " "))]
+
+
+# ---------------------------------------------------------------- Philox (P1)
+def test_philox_known_answers(golden_dir):
+    rows = _golden(golden_dir, "philox4x32_10_kat.txt", None)
+    assert len(rows) == 3
+    for r in rows:
+        vals = [int(x, 16) for x in r]
+        out = oracle.philox4x32_10(vals[0:4], vals[4:6])
+        assert [int(x) for x in out] == vals[6:10]
+
+
+# ------------------------------------------------------- triple sampler (P2)
+def test_sample_triple_distinct_in_range_and_edges():
+    rng = np.random.default_rng(1)
+    for n in range(3, 65):
+        for _ in range(200):
+            r = rng.integers(0, 2**32, 3)
+            t = oracle.sample_triple(int(r[0]), int(r[1]), int(r[2]), n)
+            assert len(set(t)) == 3 and all(0 <= x < n for x in t)
+    for n in (3, 4, 1000):
+        for r0 in (0, 2**32 - 1):
+            for r1 in (0, 2**32 - 1):
+                for r2 in (0, 2**32 - 1):
+                    t = oracle.sample_triple(r0, r1, r2, n)
+                    assert len(set(t)) == 3 and all(0 <= x < n for x in t)
+    assert {frozenset(oracle.sample_triple(*map(int, rng.integers(0, 2**32, 3)), 3)) for _ in range(50)} == {frozenset({0, 1, 2})}
+
+
+@pytest.mark.parametrize("n", [5, 7])
+def test_sample_triple_uniform_over_ordered_triples(n):
+    # chi-square over all n(n-1)(n-2) ordered triples, Philox-driven draws
+    counts = {}
+    draws = 60000
+    for h in range(draws):
+        r = oracle.philox4x32_10([h, 7, 0, 0], [0x1919, 0])
+        t = oracle.sample_triple(int(r[0]), int(r[1]), int(r[2]), n)
+        counts[t] = counts.get(t, 0) + 1
+    cells = n * (n - 1) * (n - 2)
+    assert len(counts) == cells
+    e = draws / cells
+    chi2 = sum((c - e) ** 2 / e for c in counts.values())
+    dof = cells - 1
+    assert chi2 < dof + 5 * math.sqrt(2 * dof), chi2
+
+
+def test_colex_unrank_matches_itertools():
+    n = 9
+    combos = sorted(itertools.combinations(range(n), 3), key=lambda c: (c[2], c[1], c[0]))
+    for h, c in enumerate(combos):
+        assert oracle.colex_unrank3(h, n) == c
+    assert oracle.colex_unrank3(len(combos), n) is None
+
+
+# --------------------------------------------- deprojection, planes (P3, P9)
+def test_deproject_worked_example(golden_dir):
+    (row,) = _golden(golden_dir, "spec_worked_examples.txt", "deproject")
+    u, v, z, fx, fy, cx, cy, X, Y, Z = (float(x) for x in row[1:])
+    P = oracle.deproject(int(u), int(v), z, scenegen.Intrinsics(fx, fy, cx, cy))
+    assert np.allclose(P, [X, Y, Z], atol=5e-5)
+
+
+def test_deproject_reprojection_roundtrip():
+    K = scenegen.intrinsics_for(640, 480)
+    rng = np.random.default_rng(2)
+    for _ in range(200):
+        u, v = int(rng.integers(0, 640)), int(rng.integers(0, 480))
+        z = float(rng.uniform(0.3, 8.0))
+        P = oracle.deproject(u, v, z, K).astype(np.float64)
+        assert abs(P[0] / P[2] * K.fx + K.cx - u) < 2e-3
+        assert abs(P[1] / P[2] * K.fy + K.cy - v) < 2e-3
+
+
+def test_plane_from_3pts_worked_examples(golden_dir):
+    rows = _golden(golden_dir, "spec_worked_examples.txt", "plane3")
+    for row in rows:
+        pts = [float(x) for x in row[1:10]]
+        res = oracle.plane_from_3pts(pts[0:3], pts[3:6], pts[6:9])
+        if row[11] == "collinear":
+            assert res is None
+        else:
+            assert np.allclose(res, [float(x) for x in row[11:15]], atol=1e-6)
+
+
+def test_point_plane_distance_worked_example(golden_dir):
+    (row,) = _golden(golden_dir, "spec_worked_examples.txt", "dist")
+    vals = [float(x) for x in row[1:]]
+    assert oracle.point_plane_dist(vals[0:4], vals[4:7]) == vals[7]
+
+
+def test_plane_from_3pts_random_is_consistent():
+    # all three sample points lie on their own plane (to f32 rounding), unit
+    # normal, d >= 0, and the normal is orthogonal to both edges
+    rng = np.random.default_rng(4)
+    for _ in range(500):
+        p = rng.uniform(-2, 2, (3, 3)).astype(np.float32)
+        pl = oracle.plane_from_3pts(p[0], p[1], p[2])
+        if pl is None:
+            continue
+        assert abs(np.linalg.norm(pl[:3].astype(np.float64)) - 1) < 1e-6 and pl[3] >= 0
+        for q in p:
+            assert oracle.point_plane_dist(pl, q) < 1e-5
+        e1 = (p[1] - p[0]).astype(np.float64)
+        e2 = (p[2] - p[0]).astype(np.float64)
+        nn = np.cross(e1, e2)
+        nn /= np.linalg.norm(nn)
+        assert abs(abs(nn @ pl[:3]) - 1) < 1e-5
+
+
+# ---------------------------------------------------------------- helpers
+def _region_frame(W, H, K, plane, region_mask, outlier_mask=None, outlier_offset=None):
+    """Depth of camera-frame plane n.X + d = 0 in region_mask (float32),
+    outliers displaced along the ray by outlier_offset metres."""
+    n, d = plane
+    v, u = np.mgrid[0:H, 0:W]
+    a, b = (u - K.cx) / K.fx, (v - K.cy) / K.fy
+    z = -d / (n[0] * a + n[1] * b + n[2])
+    depth = np.where(region_mask, z, 0.0)
+    if outlier_mask is not None:
+        depth = np.where(outlier_mask, depth + outlier_offset, depth)
+    labels = np.where(region_mask, 0, -1).astype(np.int32)
+    return depth.astype(np.float32), labels
+
+
+def _points(depth, labels, K, r):
+    """(X, Y, Z) float64 of region r's valid pixels, raster order (test side)."""
+    H, W = depth.shape
+    v, u = np.mgrid[0:H, 0:W]
+    m = (labels == r) & (depth > 0) & np.isfinite(depth)
+    z = depth[m].astype(np.float64)
+    return np.stack([(u[m] - K.cx) / K.fx * z, (v[m] - K.cy) / K.fy * z, z], 1)
+
+
+# ------------------------------------------------- noise-free plane (P10)
+def test_noise_free_plane_all_inliers_and_exact_refit():
+    W, H = 160, 120
+    K = scenegen.intrinsics_for(W, H)
+    depth, face, planes = scenegen.ramp(W, H, K, tilt_deg=30, azim_deg=35, d=1.5)
+    D = depth.numpy().astype(np.float32)
+    lab = np.where(D > 0, 0, -1).astype(np.int32)
+    res = oracle.ransac(D, lab, K, 1, 32, TAU, seed=0x1919, debug=True)
+    n = int(res["n_points"][0])
+    assert n == int((D > 0).sum())
+    valid_h = res["counts"][0] >= 0
+    assert np.all(res["counts"][0][valid_h] == n)
+    assert res["best_hyp"][0] == int(np.argmax(valid_h))
+    assert res["status"][0] == oracle.STATUS_OK and res["inliers"][0] == n
+    n_true, d_true = np.array(planes[0][0]), planes[0][1]
+    assert np.abs(res["n"][0] - n_true).max() < 2e-6
+    assert abs(res["d"][0] - d_true) < 2e-6
+    P = _points32(D, lab, K, 0).astype(np.float64)      # the f32 points the method uses
+    assert np.abs(res["centroid"][0] - P.mean(0)).max() < 1e-12
+
+
+# ---------------------------------------------- brute force, ENUMERATE (P11)
+def _brute_counts(P, tau):
+    """All C(n,3) planes in colex order, float64 math, and the number of
+    points with |n.p + d| < tau.  Also the distance-to-tau margin per plane."""
+    n = len(P)
+    combos = sorted(itertools.combinations(range(n), 3), key=lambda c: (c[2], c[1], c[0]))
+    idx = np.array(combos)
+    p0, p1, p2 = P[idx[:, 0]], P[idx[:, 1]], P[idx[:, 2]]
+    c = np.cross(p1 - p0, p2 - p0)
+    ln = np.linalg.norm(c, axis=1)
+    sin = ln / (np.linalg.norm(p1 - p0, axis=1) * np.linalg.norm(p2 - p0, axis=1))
+    good = sin > 1e-2              # well-conditioned: f32 and f64 planes agree to ~1e-5
+    nrm = c / np.where(ln > 0, ln, 1)[:, None]
+    d = -(nrm * p0).sum(1)
+    dist = np.abs(nrm @ P.T + d[:, None])
+    counts = (dist < tau).sum(1)
+    margin = np.abs(dist - tau).min(1)
+    return counts, good, margin
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_enumerate_matches_brute_force_max_consensus(seed):
+    rng = np.random.default_rng(seed)
+    W, H = 12, 10
+    K = scenegen.intrinsics_for(64, 48)
+    mask = np.zeros((H, W), bool)
+    sel = rng.choice(W * H, 28, replace=False)
+    mask.flat[sel] = True
+    out = np.zeros((H, W), bool)
+    out.flat[sel[:8]] = True
+    depth, lab = _region_frame(W, H, K, ((0.2, -0.3, -0.93), 1.4), mask, out,
+                               rng.uniform(0.03, 0.3, (H, W)))
+    P = _points(depth, lab, K, 0)
+    n = len(P)
+    n_h = math.comb(n, 3)
+    res = oracle.ransac(depth, lab, K, 1, n_h, TAU, seed=1, sampler=oracle.SAMPLER_ENUMERATE, debug=True)
+    cnt = res["counts"][0]
+    bc, good, margin = _brute_counts(P, TAU)
+    safe = good & (margin > 1e-4)
+    assert safe.mean() > 0.8
+    assert np.array_equal(cnt[safe], bc[safe])
+    best = int(res["best_hyp"][0])
+    assert cnt[best] == cnt.max() and np.all(cnt[:best] < cnt[best])
+    assert cnt.max() == bc[safe].max() or margin[np.argmax(bc)] <= 1e-4
+    # Philox RANSAC can never beat the exhaustive maximum
+    ph = oracle.ransac(depth, lab, K, 1, 64, TAU, seed=7)
+    assert ph["inliers"][0] <= cnt.max()
+
+
+# ------------------------------------------------ statistics, gate (P12, P14)
+def _outlier_scene(n_in, n_out, seed, W=64, H=48):
+    rng = np.random.default_rng(seed)
+    K = scenegen.intrinsics_for(W, H)
+    sel = rng.choice(W * H, n_in + n_out, replace=False)
+    mask = np.zeros((H, W), bool)
+    mask.flat[sel] = True
+    om = np.zeros((H, W), bool)
+    om.flat[sel[:n_out]] = True
+    off = rng.uniform(0.1, 0.6, (H, W)) * rng.choice([-1, 1], (H, W))
+    plane = ((0.1, -0.5, -0.86), 1.2)
+    depth, lab = _region_frame(W, H, K, plane, mask, om, off)
+    n_true = np.array(plane[0]) / np.linalg.norm(plane[0])
+    return depth, lab, K, n_true
+
+
+def test_900_inliers_100_outliers():
+    # normal within 1 degree, inlier fraction in [0.88, 0.92]; exactly
+    # 90 % is NOT accepted by Alg. 2 ℓ19 ("> 0.9"), 92 % is
+    for n_in, status in [(900, oracle.STATUS_REJECTED), (920, oracle.STATUS_OK)]:
+        depth, lab, K, n_true = _outlier_scene(n_in, 1000 - n_in, 0)
+        res = oracle.ransac(depth, lab, K, 1, 50, TAU, seed=3)
+        frac = res["inliers"][0] / res["n_points"][0]
+        assert 0.88 <= frac <= 0.92 and res["n_points"][0] == 1000
+        assert res["inliers"][0] == n_in and res["status"][0] == status
+        ang = math.degrees(math.acos(min(1.0, abs(float(res["n"][0] @ n_true)))))
+        assert ang < 1.0
+
+
+def test_500_500_rejected():
+    depth, lab, K, _ = _outlier_scene(500, 500, 1)
+    res = oracle.ransac(depth, lab, K, 1, 50, TAU, seed=3)
+    assert res["status"][0] == oracle.STATUS_REJECTED
+
+
+@pytest.mark.parametrize("n_in,n_out,status", [(9, 1, 1), (91, 9, 0), (90, 10, 1), (10, 0, 0)])
+def test_acceptance_gate_integer_cases(n_in, n_out, status):
+    # P14 / Alg. 2 ℓ19: accept iff inliers / total > 0.9, exactly
+    depth, lab, K, _ = _outlier_scene(n_in, n_out, 5)
+    n = n_in + n_out
+    res = oracle.ransac(depth, lab, K, 1, math.comb(n, 3) if n <= 12 else 256, TAU, seed=5,
+                        sampler=oracle.SAMPLER_ENUMERATE if n <= 12 else oracle.SAMPLER_PHILOX)
+    assert res["inliers"][0] == n_in and res["n_points"][0] == n
+    assert res["status"][0] == status
+
+
+def test_too_few_and_degenerate():
+    K = scenegen.intrinsics_for(64, 48)
+    depth = np.full((48, 64), 1.5, np.float32)
+    lab = np.full((48, 64), -1, np.int32)
+    lab[3, 4] = lab[7, 9] = 0                   # 2 points -> TOO_FEW
+    lab[10, 5:20] = 1                           # one row, constant depth -> collinear
+    res = oracle.ransac(depth, lab, K, 3, 16, TAU, seed=1)
+    assert list(res["status"]) == [oracle.STATUS_TOO_FEW, oracle.STATUS_DEGENERATE, oracle.STATUS_TOO_FEW]
+    assert list(res["n_points"]) == [2, 15, 0]
+
+
+def test_bernoulli_failure_rate():
+    # with inlier ratio w and I iterations, a run fails (no all-inlier
+    # sample) with probability (1 - p3)^I, p3 = C(n_in,3)/C(n,3) (sampling
+    # without replacement).  Failure <=> best count < n_in here.
+    depth, lab, K, _ = _outlier_scene(20, 20, 9, W=16, H=12)
+    n_in, n = 20, 40
+    p3 = math.comb(n_in, 3) / math.comb(n, 3)
+    I, trials = 10, 300
+    fails = 0
+    for s in range(trials):
+        res = oracle.ransac(depth, lab, K, 1, I, TAU, seed=1000 + s)
+        fails += int(res["inliers"][0] < n_in)
+    p = (1 - p3) ** I
+    mu, sd = trials * p, math.sqrt(trials * p * (1 - p))
+    assert abs(fails - mu) < 4.5 * sd, (fails, mu, sd)
+
+
+# ------------------------------------------------------------- refit (P13)
+def test_refit_matches_library_eigh():
+    rng = np.random.default_rng(8)
+    for _ in range(50):
+        n = rng.integers(3, 400)
+        basis = rng.standard_normal((3, 3))
+        pts = rng.standard_normal((n, 2)) @ basis[:2] * rng.uniform(0.1, 2) + rng.uniform(-3, 3, 3)
+        pts += 1e-3 * rng.standard_normal((n, 3)) * rng.uniform(0, 1)
+        out = oracle.refit_plane(pts)
+        c = pts.mean(0)
+        w, V = np.linalg.eigh((pts - c).T @ (pts - c))
+        nv = V[:, 0]
+        dd = -nv @ c
+        if dd < 0:
+            nv, dd = -nv, -dd
+        assert np.abs(out[4:7] - c).max() < 1e-12
+        assert np.abs(out[0:3] - nv).max() < 1e-8 and abs(out[3] - dd) < 1e-8
+
+
+def _points32(depth, labels, K, r):
+    """Region r's points in f32 with the prescribed deprojection order (numpy
+    float32 arithmetic is IEEE single, no contraction)."""
+    H, W = depth.shape
+    v, u = np.mgrid[0:H, 0:W]
+    m = (labels == r) & (depth > 0) & np.isfinite(depth)
+    f32 = np.float32
+    z = depth[m].astype(f32)
+    ifx, ify = f32(1) / f32(K.fx), f32(1) / f32(K.fy)
+    X = ((u[m].astype(f32) - f32(K.cx)) * ifx) * z
+    Y = ((v[m].astype(f32) - f32(K.cy)) * ify) * z
+    return np.stack([X, Y, z], 1)
+
+
+def _hyp_plane(P32, r, h, seed, frame=0):
+    rnd = oracle.philox4x32_10([h, r, frame, 0], [seed & 0xFFFFFFFF, seed >> 32])
+    i = oracle.sample_triple(int(rnd[0]), int(rnd[1]), int(rnd[2]), len(P32))
+    return oracle.plane_from_3pts(P32[i[0]], P32[i[1]], P32[i[2]])
+
+
+def test_refit_minimises_squared_error_over_winner_inliers():
+    # total least squares: over the winner's inlier set S the refit plane has
+    # sum d^2 <= that of the 3-point winner (and of any plane)
+    fr = scenegen.make_config("C2", W=160, H=120)
+    D, lab, K = fr["depth"].numpy(), fr["labels"].numpy(), fr["K"]
+    res = oracle.ransac(D, lab, K, fr["n_regions"], 32, TAU, seed=0x1919)
+    checked = 0
+    for r in range(fr["n_regions"]):
+        if res["status"][r] > 1:
+            continue
+        P32 = _points32(D, lab, K, r)
+        pl = _hyp_plane(P32, r, int(res["best_hyp"][r]), 0x1919)
+        P = P32.astype(np.float64)
+        d3 = np.abs(P @ pl[:3].astype(np.float64) + float(pl[3]))
+        S = d3 < TAU
+        assert abs(int(S.sum()) - int(res["inliers"][r])) <= 2
+        ssq_refit = ((P[S] @ res["n"][r] + res["d"][r]) ** 2).sum()
+        ssq_3pt = (d3[S] ** 2).sum()
+        assert ssq_refit <= ssq_3pt * (1 + 1e-9)
+        if int(S.sum()) == int(res["inliers"][r]):
+            assert np.abs(res["centroid"][r] - P[S].mean(0)).max() < 1e-9
+        checked += 1
+    assert checked >= fr["n_regions"] // 2
+
+
+# ------------------------------------------------------ selection, determinism
+def test_select_modes_and_determinism():
+    fr = scenegen.make_config("C1n")
+    D, lab, K = fr["depth"].numpy(), fr["labels"].numpy(), fr["K"]
+    a = oracle.ransac(D, lab, K, 4, 64, TAU, seed=0x1919, debug=True)
+    b = oracle.ransac(D, lab, K, 4, 64, TAU, seed=0x1919, debug=True)
+    for k in a:
+        assert np.array_equal(a[k], b[k])
+    for r in range(4):
+        cnt, err = a["counts"][r], a["errq_all"][r]
+        ok = cnt >= 0
+        h = a["best_hyp"][r]
+        assert cnt[h] == cnt[ok].max() and np.all(cnt[:h] < cnt[h])
+        assert a["errq"][r] == err[h]
+    e = oracle.ransac(D, lab, K, 4, 64, TAU, seed=0x1919, select=oracle.SELECT_ERROR, debug=True)
+    for r in range(4):
+        err, cnt = e["errq_all"][r], e["counts"][r]
+        ok = cnt >= 0
+        h = e["best_hyp"][r]
+        assert err[h] == err[ok].min() and np.all((err[:h] > err[h]) | ~ok[:h])
+    c = oracle.ransac(D, lab, K, 4, 64, TAU, seed=0x1919, frame_id=1, debug=True)
+    assert not np.array_equal(a["counts"], c["counts"])
+
+
+def test_errq_is_fixed_point_sum_of_distances():
+    # Q12: error = sum_i rint(min(d_i, 64) * 2^24) over ALL points (Alg. 2
+    # ℓ11 sits outside the inlier test).  Compare every hypothesis' errq with
+    # a float64 sum of distances to its plane: the gap is bounded by n/2 units
+    # of rounding plus the f32 error of each distance.
+    fr = scenegen.make_config("C1n")
+    D, lab, K = fr["depth"].numpy(), fr["labels"].numpy(), fr["K"]
+    res = oracle.ransac(D, lab, K, 4, 16, TAU, seed=3, debug=True)
+    for r in range(4):
+        P32 = _points32(D, lab, K, r)
+        P = P32.astype(np.float64)
+        for h in range(16):
+            pl = _hyp_plane(P32, r, h, 3)
+            if pl is None:
+                assert res["counts"][r][h] == -1
+                continue
+            dist = np.abs(P @ pl[:3].astype(np.float64) + float(pl[3]))
+            want = np.minimum(dist, 64.0).sum()
+            got = float(res["errq_all"][r][h]) / 2**24
+            assert abs(got - want) <= len(P) * (0.5 / 2**24 + 1e-6 * (1 + np.abs(P).max())), (r, h, got, want)
+            assert res["counts"][r][h] == int((dist < TAU).sum()) or np.min(np.abs(dist - TAU)) < 1e-5
