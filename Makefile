@@ -1,0 +1,26 @@
+# Builds the product library (CUDA, sm_100a) and the oracle (plain C, test infrastructure).
+NVCC     ?= /usr/local/cuda/bin/nvcc
+PKG      := paper_2411_01919_b200
+SRC      := $(wildcard $(PKG)/csrc/*.cu)
+HDR      := $(wildcard $(PKG)/csrc/*.cuh $(PKG)/csrc/*.h) include/pmap.h
+LIB      := $(PKG)/libpmap.so
+# --fmad=false: no implicit FMA contraction; every fused multiply-add the
+# method prescribes is written as __fmaf_rn.
+NVFLAGS  := -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -lineinfo --fmad=false \
+            -Xcompiler -fPIC,-fvisibility=hidden -shared -Iinclude
+
+all: $(LIB) oracle/liboracle.so
+
+$(LIB): $(SRC) $(HDR)
+	$(NVCC) $(NVFLAGS) -o $@.tmp $(SRC) && mv $@.tmp $@
+
+oracle/liboracle.so: oracle/oracle.c
+	gcc -O2 -std=c11 -fPIC -shared -ffp-contract=off -fno-fast-math -fvisibility=hidden -o $@ $< -lm
+
+ptxas:
+	$(NVCC) $(NVFLAGS) -Xptxas -v -o /tmp/pmap_ptxas.so $(SRC) 2>&1 | grep -E "Function properties|registers|spill|smem|Compiling entry" | sed 's/ptxas info    ://'
+
+clean:
+	rm -f $(LIB) oracle/liboracle.so
+
+.PHONY: all clean ptxas

@@ -1,0 +1,210 @@
+/*
+ * pmap.h — C ABI of the B200-native hot path of arXiv 2411.01919
+ * ("real-time planar semantic mapping"): iterated Perona–Malik anisotropic
+ * diffusion of a depth frame, the per-pixel normal image fused into the last
+ * diffusion pass, and batched RANSAC plane fitting over every labelled region.
+ *
+ * Citations: "P:n" = line n of the paper text, "S:n" = line n of
+ * SPEC.md, "Qk" = reading k in DESIGN.md §3 (where the paper is silent or
+ * ambiguous).
+ *
+ * Conventions (all calls)
+ *  - Every pointer is a DEVICE pointer unless marked "host".  The caller owns
+ *    every buffer, including the workspace; the library allocates nothing.
+ *  - Work is enqueued asynchronously on `stream` (a cudaStream_t; NULL = the
+ *    legacy default stream).  No call synchronises the host except the
+ *    *_host pipeline entry, which synchronises its own stream before return.
+ *  - Frames are row-major f32 [H][W] in metres; u = column, v = row (Q25).
+ *    A depth value is VALID iff it is > 0 and finite (Q4).  Batched
+ *    calls take n_frames contiguous frames [B][H][W].
+ *  - Argument errors are detected before any launch and return
+ *    PM_ERR_INVALID_ARGUMENT; too-small workspaces return PM_ERR_WORKSPACE;
+ *    a failed launch returns PM_ERR_CUDA (asynchronous faults surface at the
+ *    caller's next synchronisation).  Per-region RANSAC failures are
+ *    statuses in pm_plane, not errors.
+ *  - Limits: 3 <= W, H <= 65535; 0 <= n_regions <= 65536; 1 <= n_hyp <= 4096;
+ *    1 <= n_frames <= 65535.
+ *  - Calls are re-entrant and thread-safe (the only global state is a
+ *    one-time kernel-attribute setup guarded by std::call_once).
+ */
+#ifndef PMAP_H_
+#define PMAP_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define PM_API __attribute__((visibility("default")))
+#else
+#define PM_API
+#endif
+
+typedef struct CUstream_st* pm_stream_t;   /* == cudaStream_t */
+
+typedef enum {
+    PM_OK = 0,
+    PM_ERR_INVALID_ARGUMENT = 1,
+    PM_ERR_WORKSPACE = 2,
+    PM_ERR_UNSUPPORTED = 3,
+    PM_ERR_CUDA = 4
+} pm_status;
+
+/* Pinhole intrinsics K ("camera intrinsic matrix"; Q24): fx, fy > 0
+ * and finite; cx, cy in pixels.  Always passed by HOST pointer. */
+typedef struct { float fx, fy, cx, cy; } pm_intrinsics;
+
+/* One fitted plane per (frame, region): n.X + d = 0 in the camera frame,
+ * |n| = 1, d >= 0 (metres); centroid = mean of the refit inliers (Q22).
+ * inliers = best hypothesis' inlier count (Alg. 2 ℓ16), n_points = valid
+ * labelled pixels of the region, best_hyp = winning hypothesis index or -1,
+ * status = PM_PLANE_*; sum_dist = the winner's total distance Σ min(d,64)
+ * (Alg. 2 ℓ11, error), from the exact fixed-point sum, informative. 48 bytes. */
+typedef struct {
+    float n[3];
+    float d;
+    float centroid[3];
+    int32_t inliers;
+    int32_t n_points;
+    int32_t best_hyp;
+    int32_t status;
+    float sum_dist;
+} pm_plane;
+
+enum {
+    PM_PLANE_OK = 0,          /* 10 * inliers > 9 * n_points (Alg. 2 ℓ19) */
+    PM_PLANE_REJECTED = 1,    /* gate failed: outliers >= 10 %            */
+    PM_PLANE_TOO_FEW = 2,     /* n_points < 3                              */
+    PM_PLANE_DEGENERATE = 3   /* every hypothesis collinear (Q18)                  */
+};
+
+/* ---------------------------------------------------------------------- */
+/* adf_filter — Algorithm 1: N Jacobi sweeps of
+ *   I_p <- I_p + lambda * c_p * lap(I_p),  c_p = exp(-|grad I_p|^2 / kappa^2)
+ * (ℓ2-8; Eq. 1; central-difference gradient Q3; 5-point Laplacian;
+ * zero-flux rule Q4: an out-of-image or invalid neighbour takes the centre
+ * value; invalid pixels are copied bit for bit), then, if normals_out is not
+ * NULL, the normal image of the result (ℓ9-13, see normals_from_depth) fused
+ * into the last diffusion pass.
+ *   depth_in   [B][H][W] f32, read only; must not overlap depth_out.
+ *   depth_out  [B][H][W] f32, written (I_smooth).
+ *   K          host pointer; required iff normals_out != NULL.
+ *   lambda     gamma of Alg. 1, 0 < lambda <= 0.25 (stability).
+ *   kappa      k of Alg. 1 in metres, > 0.
+ *   iters      N >= 0 (N = 0 copies depth_in).
+ *   normals_out [B][3][H][W] f32 (SoA: nx plane, ny plane, nz plane) or NULL.
+ *   workspace  >= pm_adf_workspace_bytes(W, H, n_frames) bytes, 256-B aligned.
+ * The result is bitwise independent of n_frames and of the blocking depth. */
+PM_API pm_status pm_adf_filter(const float* depth_in, float* depth_out, int32_t W, int32_t H,
+                               const pm_intrinsics* K, float lambda, float kappa, int32_t iters,
+                               float* normals_out, void* workspace, size_t ws_bytes,
+                               pm_stream_t stream);
+PM_API pm_status pm_adf_filter_batched(const float* depth_in, float* depth_out, int32_t W, int32_t H,
+                                       int32_t n_frames, const pm_intrinsics* K, float lambda,
+                                       float kappa, int32_t iters, float* normals_out,
+                                       void* workspace, size_t ws_bytes, pm_stream_t stream);
+PM_API size_t pm_adf_workspace_bytes(int32_t W, int32_t H, int32_t n_frames);
+
+/* Tuning / test knobs for adf (results do not depend on them). */
+typedef struct {
+    int32_t iters_per_pass;   /* temporal blocking depth T per HBM pass; 0 = default */
+} pm_adf_options;
+PM_API pm_status pm_adf_filter_ex(const float* depth_in, float* depth_out, int32_t W, int32_t H,
+                                  int32_t n_frames, const pm_intrinsics* K, float lambda,
+                                  float kappa, int32_t iters, float* normals_out,
+                                  void* workspace, size_t ws_bytes, const pm_adf_options* opt,
+                                  pm_stream_t stream);
+
+/* ---------------------------------------------------------------------- */
+/* normals_from_depth — Alg. 1 ℓ9-13, Eq. 2 read
+ * geometrically (Q7): with 3x3 Sobel gradients of Z normalised by 1/8 and
+ * clamp-to-edge indexing (Q8),
+ *   m = ( fx Gx, fy Gy, -(Z + (u - cx) Gx + (v - cy) Gy) ),  n = m / |m|
+ * (the tangent cross product dP/du x dP/dv of P = Z K^-1 [u v 1]^T; it faces
+ * the camera).  n = (0,0,0) if any pixel of the clamped 3x3 window is
+ * invalid (Q9).  depth [B][H][W] f32; normals_out [B][3][H][W] f32. */
+PM_API pm_status pm_normals_from_depth(const float* depth, int32_t W, int32_t H,
+                                       const pm_intrinsics* K, float* normals_out,
+                                       pm_stream_t stream);
+PM_API pm_status pm_normals_from_depth_batched(const float* depth, int32_t W, int32_t H,
+                                               int32_t n_frames, const pm_intrinsics* K,
+                                               float* normals_out, pm_stream_t stream);
+
+/* ---------------------------------------------------------------------- */
+/* ransac_planes — Algorithm 2, batched over every region of every
+ * frame.  For region r of frame f (f = first_frame_id + batch index):
+ *   P  = its valid labelled pixels in raster order, deprojected in f32 as
+ *        X = (((float)u - cx) * (1/fx)) * z, Y likewise, Z = z  (ℓ2-3)
+ *   hypothesis h (0 <= h < n_hyp): Philox4x32-10 of counter {h, r, f, 0},
+ *        key {lo32(seed), hi32(seed)} -> 3 distinct indices (Q17) -> f32 plane
+ *        (ℓ6-7); collinear samples are invalid (Q18)
+ *   score: inliers_h = #{ |n.p + d| < inlier_thresh } (ℓ9-13, strict, Q14)
+ *   select: argmax inliers, ties to the lowest h (Q11)
+ *   refit: fp64 total least squares over the winner's inliers (Q19)
+ *   gate: PM_PLANE_OK iff 10 * inliers > 9 * n_points (ℓ19, Q15).
+ * The exact float32 operation sequence is DESIGN.md §3 (shared with the
+ * oracle by specification, not by code).
+ *   depth          [B][H][W] f32 (raw or filtered, Q10).
+ *   region_labels  [B][H][W] int32; labels outside [0, n_regions) are ignored.
+ *   planes_out     [B][n_regions] pm_plane.
+ *   inlier_thresh  tau in metres, > 0 and finite.
+ *   workspace      >= pm_ransac_workspace_bytes(W, H, n_regions, n_hyp, n_frames).
+ * Results are bitwise independent of batching and launch geometry. */
+PM_API pm_status pm_ransac_planes(const float* depth, int32_t W, int32_t H, const pm_intrinsics* K,
+                                  const int32_t* region_labels, int32_t n_regions, int32_t n_hyp,
+                                  float inlier_thresh, uint64_t seed, pm_plane* planes_out,
+                                  void* workspace, size_t ws_bytes, pm_stream_t stream);
+PM_API pm_status pm_ransac_planes_batched(const float* depth, int32_t W, int32_t H, int32_t n_frames,
+                                          uint32_t first_frame_id, const pm_intrinsics* K,
+                                          const int32_t* region_labels, int32_t n_regions,
+                                          int32_t n_hyp, float inlier_thresh, uint64_t seed,
+                                          pm_plane* planes_out, void* workspace, size_t ws_bytes,
+                                          pm_stream_t stream);
+PM_API size_t pm_ransac_workspace_bytes(int32_t W, int32_t H, int32_t n_regions, int32_t n_hyp,
+                                        int32_t n_frames);
+
+/* Test / paper-literal options for ransac (NEXT-1 rows of SURVEY §8(f)). */
+enum { PM_SAMPLER_PHILOX = 0, PM_SAMPLER_ENUMERATE = 1 };   /* ENUMERATE: h -> h-th 3-combination, colex */
+enum { PM_SELECT_COUNT = 0, PM_SELECT_ERROR = 1 };          /* ERROR: argmin Σd as printed       */
+typedef struct {
+    int32_t sampler;          /* PM_SAMPLER_*                                          */
+    int32_t select;           /* PM_SELECT_*                                           */
+    int32_t* counts_out;      /* nullable device [B][n_regions][n_hyp]: inliers per h,
+                                 -1 = invalid hypothesis                                */
+    uint64_t* errq_out;       /* nullable device [B][n_regions][n_hyp]: Σ rint(min(d,64)
+                                 * 2^24) per h (required work for PM_SELECT_ERROR)     */
+} pm_ransac_options;
+PM_API pm_status pm_ransac_planes_ex(const float* depth, int32_t W, int32_t H, int32_t n_frames,
+                                     uint32_t first_frame_id, const pm_intrinsics* K,
+                                     const int32_t* region_labels, int32_t n_regions,
+                                     int32_t n_hyp, float inlier_thresh, uint64_t seed,
+                                     pm_plane* planes_out, void* workspace, size_t ws_bytes,
+                                     const pm_ransac_options* opt, pm_stream_t stream);
+
+/* ---------------------------------------------------------------------- */
+/* Whole per-frame path (adf_filter with fused normals, then ransac_planes on
+ * the FILTERED depth, Q10) for n_frames device-resident frames.
+ * depth_out, normals_out, planes_out as above; workspace >=
+ * pm_pipeline_workspace_bytes(...). */
+PM_API pm_status pm_process_frames(const float* depth_in, const int32_t* region_labels,
+                                   int32_t W, int32_t H, int32_t n_frames, uint32_t first_frame_id,
+                                   const pm_intrinsics* K, float lambda, float kappa, int32_t iters,
+                                   int32_t n_regions, int32_t n_hyp, float inlier_thresh,
+                                   uint64_t seed, float* depth_out, float* normals_out,
+                                   pm_plane* planes_out, void* workspace, size_t ws_bytes,
+                                   pm_stream_t stream);
+PM_API size_t pm_pipeline_workspace_bytes(int32_t W, int32_t H, int32_t n_regions, int32_t n_hyp,
+                                          int32_t n_frames);
+
+/* Human-readable status. */
+PM_API const char* pm_status_string(pm_status s);
+/* ABI version (major * 10000 + minor * 100 + patch). */
+PM_API int32_t pm_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PMAP_H_ */

@@ -1,0 +1,250 @@
+"""B200-native hot path of arXiv 2411.01919 (planar semantic mapping):
+anisotropic diffusion + fused normals (Alg. 1) and batched RANSAC plane
+fitting (Alg. 2), as hand-written sm_100a CUDA kernels behind the C ABI of
+``include/pmap.h`` (``libpmap.so``).
+
+This module is argument marshalling only: it passes device pointers of torch
+tensors and the current CUDA stream to the C ABI; every step of the path runs
+in the library's kernels.  There is no CPU fallback: importing this package
+without the built library raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import NamedTuple
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libpmap.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} is missing: build it with `make` (or __graft_entry__.build()); "
+                      "this package has no CPU fallback")
+
+_lib = ctypes.CDLL(LIB_PATH)
+
+STATUS_OK, STATUS_REJECTED, STATUS_TOO_FEW, STATUS_DEGENERATE = 0, 1, 2, 3
+SAMPLER_PHILOX, SAMPLER_ENUMERATE = 0, 1
+SELECT_COUNT, SELECT_ERROR = 0, 1
+PLANE_WORDS = 12          # sizeof(pm_plane) / 4
+
+
+class pm_intrinsics(ctypes.Structure):
+    _fields_ = [("fx", ctypes.c_float), ("fy", ctypes.c_float), ("cx", ctypes.c_float), ("cy", ctypes.c_float)]
+
+
+class pm_adf_options(ctypes.Structure):
+    _fields_ = [("iters_per_pass", ctypes.c_int32)]
+
+
+class pm_ransac_options(ctypes.Structure):
+    _fields_ = [("sampler", ctypes.c_int32), ("select", ctypes.c_int32),
+                ("counts_out", ctypes.c_void_p), ("errq_out", ctypes.c_void_p)]
+
+
+_P, _I32, _U32, _U64, _F32, _SZ = (ctypes.c_void_p, ctypes.c_int32, ctypes.c_uint32, ctypes.c_uint64,
+                                   ctypes.c_float, ctypes.c_size_t)
+_KP = ctypes.POINTER(pm_intrinsics)
+_lib.pm_status_string.restype = ctypes.c_char_p
+_lib.pm_status_string.argtypes = [ctypes.c_int]
+_lib.pm_version.restype = _I32
+_lib.pm_adf_workspace_bytes.restype = _SZ
+_lib.pm_adf_workspace_bytes.argtypes = [_I32, _I32, _I32]
+_lib.pm_ransac_workspace_bytes.restype = _SZ
+_lib.pm_ransac_workspace_bytes.argtypes = [_I32, _I32, _I32, _I32, _I32]
+_lib.pm_pipeline_workspace_bytes.restype = _SZ
+_lib.pm_pipeline_workspace_bytes.argtypes = [_I32, _I32, _I32, _I32, _I32]
+_lib.pm_adf_filter.argtypes = [_P, _P, _I32, _I32, _KP, _F32, _F32, _I32, _P, _P, _SZ, _P]
+_lib.pm_adf_filter_batched.argtypes = [_P, _P, _I32, _I32, _I32, _KP, _F32, _F32, _I32, _P, _P, _SZ, _P]
+_lib.pm_adf_filter_ex.argtypes = [_P, _P, _I32, _I32, _I32, _KP, _F32, _F32, _I32, _P, _P, _SZ,
+                                  ctypes.POINTER(pm_adf_options), _P]
+_lib.pm_normals_from_depth.argtypes = [_P, _I32, _I32, _KP, _P, _P]
+_lib.pm_normals_from_depth_batched.argtypes = [_P, _I32, _I32, _I32, _KP, _P, _P]
+_lib.pm_ransac_planes.argtypes = [_P, _I32, _I32, _KP, _P, _I32, _I32, _F32, _U64, _P, _P, _SZ, _P]
+_lib.pm_ransac_planes_batched.argtypes = [_P, _I32, _I32, _I32, _U32, _KP, _P, _I32, _I32, _F32, _U64,
+                                          _P, _P, _SZ, _P]
+_lib.pm_ransac_planes_ex.argtypes = [_P, _I32, _I32, _I32, _U32, _KP, _P, _I32, _I32, _F32, _U64, _P, _P, _SZ,
+                                     ctypes.POINTER(pm_ransac_options), _P]
+_lib.pm_process_frames.argtypes = [_P, _P, _I32, _I32, _I32, _U32, _KP, _F32, _F32, _I32, _I32, _I32, _F32,
+                                   _U64, _P, _P, _P, _P, _SZ, _P]
+for _fn in ("pm_adf_filter", "pm_adf_filter_batched", "pm_adf_filter_ex", "pm_normals_from_depth",
+            "pm_normals_from_depth_batched", "pm_ransac_planes", "pm_ransac_planes_batched",
+            "pm_ransac_planes_ex", "pm_process_frames"):
+    getattr(_lib, _fn).restype = ctypes.c_int
+
+EXPORTED = ("pm_adf_filter", "pm_adf_filter_batched", "pm_adf_filter_ex", "pm_adf_workspace_bytes",
+            "pm_normals_from_depth", "pm_normals_from_depth_batched", "pm_ransac_planes",
+            "pm_ransac_planes_batched", "pm_ransac_planes_ex", "pm_ransac_workspace_bytes",
+            "pm_process_frames", "pm_pipeline_workspace_bytes", "pm_status_string", "pm_version")
+
+
+class PMError(RuntimeError):
+    pass
+
+
+def _check(rc: int) -> None:
+    if rc != 0:
+        raise PMError(f"pmap: {_lib.pm_status_string(rc).decode()} (status {rc})")
+
+
+def version() -> int:
+    return int(_lib.pm_version())
+
+
+def _K(K) -> pm_intrinsics:
+    if isinstance(K, pm_intrinsics):
+        return K
+    if isinstance(K, (tuple, list)):
+        return pm_intrinsics(*[float(x) for x in K])
+    return pm_intrinsics(float(K.fx), float(K.fy), float(K.cx), float(K.cy))
+
+
+def _frames(t: torch.Tensor, dtype) -> tuple:
+    if not t.is_cuda:
+        raise PMError("pmap: tensors must live on a CUDA device")
+    if t.dtype != dtype or not t.is_contiguous():
+        raise PMError(f"pmap: expected a contiguous {dtype} tensor")
+    if t.dim() == 2:
+        return 1, t.shape[0], t.shape[1]
+    if t.dim() == 3:
+        return t.shape[0], t.shape[1], t.shape[2]
+    raise PMError("pmap: expected [H, W] or [B, H, W]")
+
+
+def _stream(t: torch.Tensor) -> int:
+    return torch.cuda.current_stream(t.device).cuda_stream
+
+
+def _workspace(nbytes: int, device) -> torch.Tensor:
+    return torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=device)
+
+
+def adf_workspace_bytes(W: int, H: int, n_frames: int = 1) -> int:
+    return int(_lib.pm_adf_workspace_bytes(W, H, n_frames))
+
+
+def ransac_workspace_bytes(W: int, H: int, n_regions: int, n_hyp: int, n_frames: int = 1) -> int:
+    return int(_lib.pm_ransac_workspace_bytes(W, H, n_regions, n_hyp, n_frames))
+
+
+def pipeline_workspace_bytes(W: int, H: int, n_regions: int, n_hyp: int, n_frames: int = 1) -> int:
+    return int(_lib.pm_pipeline_workspace_bytes(W, H, n_regions, n_hyp, n_frames))
+
+
+def adf_filter(depth: torch.Tensor, K, lam: float, kappa: float, iters: int, normals: bool = True,
+               iters_per_pass: int = 0, out: torch.Tensor = None, normals_out: torch.Tensor = None,
+               workspace: torch.Tensor = None):
+    """Alg. 1 on [H, W] or [B, H, W] f32 depth (metres, CUDA).
+    Returns (I_smooth, normals [.., 3, H, W] or None)."""
+    B, H, W = _frames(depth, torch.float32)
+    out = torch.empty_like(depth) if out is None else out
+    nrm = None
+    if normals:
+        shape = (3, H, W) if depth.dim() == 2 else (B, 3, H, W)
+        nrm = torch.empty(shape, dtype=torch.float32, device=depth.device) if normals_out is None else normals_out
+    ws = workspace if workspace is not None else _workspace(adf_workspace_bytes(W, H, B), depth.device)
+    opt = pm_adf_options(int(iters_per_pass))
+    _check(_lib.pm_adf_filter_ex(depth.data_ptr(), out.data_ptr(), W, H, B, ctypes.byref(_K(K)), float(lam),
+                                 float(kappa), int(iters), nrm.data_ptr() if nrm is not None else None,
+                                 ws.data_ptr(), ws.numel(), ctypes.byref(opt), _stream(depth)))
+    return out, nrm
+
+
+def normals_from_depth(depth: torch.Tensor, K, out: torch.Tensor = None) -> torch.Tensor:
+    """Alg. 1 ℓ9-13 on [H, W] or [B, H, W] f32 depth -> [.., 3, H, W]."""
+    B, H, W = _frames(depth, torch.float32)
+    shape = (3, H, W) if depth.dim() == 2 else (B, 3, H, W)
+    out = torch.empty(shape, dtype=torch.float32, device=depth.device) if out is None else out
+    _check(_lib.pm_normals_from_depth_batched(depth.data_ptr(), W, H, B, ctypes.byref(_K(K)), out.data_ptr(),
+                                              _stream(depth)))
+    return out
+
+
+class Planes(NamedTuple):
+    """Views of a pm_plane table [.., R] (48-byte records)."""
+    raw: torch.Tensor        # int32 [.., R, 12]
+
+    @property
+    def n(self):
+        return self.raw[..., 0:3].view(torch.float32)
+
+    @property
+    def d(self):
+        return self.raw[..., 3].view(torch.float32)
+
+    @property
+    def centroid(self):
+        return self.raw[..., 4:7].view(torch.float32)
+
+    @property
+    def inliers(self):
+        return self.raw[..., 7]
+
+    @property
+    def n_points(self):
+        return self.raw[..., 8]
+
+    @property
+    def best_hyp(self):
+        return self.raw[..., 9]
+
+    @property
+    def status(self):
+        return self.raw[..., 10]
+
+    @property
+    def sum_dist(self):
+        return self.raw[..., 11].view(torch.float32)
+
+
+def ransac_planes(depth: torch.Tensor, K, labels: torch.Tensor, n_regions: int, n_hyp: int, tau: float,
+                  seed: int, first_frame_id: int = 0, sampler: int = SAMPLER_PHILOX,
+                  select: int = SELECT_COUNT, debug: bool = False, out: torch.Tensor = None,
+                  workspace: torch.Tensor = None):
+    """Alg. 2 over every region of every frame.  Returns Planes
+    (and, with debug=True, per-hypothesis counts / errq tensors [.., R, n_hyp])."""
+    B, H, W = _frames(depth, torch.float32)
+    if tuple(labels.shape) != tuple(depth.shape):
+        raise PMError("pmap: labels must have the depth's shape")
+    _frames(labels, torch.int32)
+    lead = () if depth.dim() == 2 else (B,)
+    out = torch.empty(lead + (n_regions, PLANE_WORDS), dtype=torch.int32, device=depth.device) if out is None else out
+    ws = workspace if workspace is not None else _workspace(
+        ransac_workspace_bytes(W, H, n_regions, n_hyp, B), depth.device)
+    counts = errq = None
+    if debug:
+        counts = torch.empty(lead + (n_regions, n_hyp), dtype=torch.int32, device=depth.device)
+        errq = torch.empty(lead + (n_regions, n_hyp), dtype=torch.int64, device=depth.device)
+    opt = pm_ransac_options(int(sampler), int(select), counts.data_ptr() if debug else None,
+                            errq.data_ptr() if debug else None)
+    _check(_lib.pm_ransac_planes_ex(depth.data_ptr(), W, H, B, int(first_frame_id), ctypes.byref(_K(K)),
+                                    labels.data_ptr(), int(n_regions), int(n_hyp), float(tau),
+                                    int(seed) & (2**64 - 1), out.data_ptr(), ws.data_ptr(), ws.numel(),
+                                    ctypes.byref(opt), _stream(depth)))
+    planes = Planes(out)
+    return (planes, counts, errq) if debug else planes
+
+
+def process_frames(depth: torch.Tensor, labels: torch.Tensor, K, lam: float, kappa: float, iters: int,
+                   n_regions: int, n_hyp: int, tau: float, seed: int, first_frame_id: int = 0,
+                   depth_out: torch.Tensor = None, normals_out: torch.Tensor = None,
+                   planes_out: torch.Tensor = None, workspace: torch.Tensor = None):
+    """The whole per-frame path in one C-ABI call (pm_process_frames):
+    adf_filter with fused normals, then ransac_planes on the filtered depth."""
+    B, H, W = _frames(depth, torch.float32)
+    _frames(labels, torch.int32)
+    lead = () if depth.dim() == 2 else (B,)
+    dev = depth.device
+    depth_out = torch.empty_like(depth) if depth_out is None else depth_out
+    normals_out = torch.empty(lead + (3, H, W), dtype=torch.float32, device=dev) if normals_out is None else normals_out
+    planes_out = torch.empty(lead + (n_regions, PLANE_WORDS), dtype=torch.int32, device=dev) if planes_out is None else planes_out
+    ws = workspace if workspace is not None else _workspace(
+        pipeline_workspace_bytes(W, H, n_regions, n_hyp, B), dev)
+    _check(_lib.pm_process_frames(depth.data_ptr(), labels.data_ptr(), W, H, B, int(first_frame_id),
+                                  ctypes.byref(_K(K)), float(lam), float(kappa), int(iters), int(n_regions),
+                                  int(n_hyp), float(tau), int(seed) & (2**64 - 1), depth_out.data_ptr(),
+                                  normals_out.data_ptr(), planes_out.data_ptr(), ws.data_ptr(), ws.numel(),
+                                  _stream(depth)))
+    return depth_out, normals_out, Planes(planes_out)

@@ -1,0 +1,224 @@
+// compact.cu — Alg. 2 ℓ2 "Extract depth values within c from I" for
+// every region of every frame at once: a stable, deterministic compaction of
+// the valid labelled pixels into per-region lists in raster order (the order
+// hypothesis indices refer to).
+//
+//   count   : each warp owns a sub-tile of `sub_tile` consecutive pixels and
+//             counts (region, sub-tile) occurrences.  Labels are spatially
+//             coherent, so the warp keeps a run-length cache (current label,
+//             running count) in registers and touches memory only when the
+//             label changes; a step with several labels falls back to
+//             __match_any_sync groups.  hist entries are owned by one warp:
+//             no atomics, no ordering dependence.
+//   scan    : per (frame, region) exclusive prefix over sub-tiles -> counts;
+//             per frame exclusive prefix over regions -> region offsets.
+//   scatter : the same warp walk, writing packed (u, v, z) points to
+//             region_off + prefix + rank-in-step.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+#include "internal.h"
+
+namespace pm {
+
+namespace {
+
+constexpr unsigned kFull = 0xFFFFFFFFu;
+constexpr int kWarpsPerBlock = 8;
+
+PM_DEVINL unsigned lanemask_lt() {
+    unsigned m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+// Label of pixel i for region purposes: -1 unless 0 <= label < R and depth valid.
+PM_DEVINL int pixel_label(const float* __restrict__ depth, const int32_t* __restrict__ labels,
+                          size_t i, size_t end, int R) {
+    if (i >= end) return -1;
+    const int l = __ldg(labels + i);
+    const float z = __ldg(depth + i);
+    return (valid_depth(z) && (unsigned)l < (unsigned)R) ? l : -1;
+}
+
+__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+compact_count_kernel(const float* __restrict__ depth, const int32_t* __restrict__ labels,
+                     int WH, int R, int sub_tile, int n_sub, int32_t* __restrict__ hist) {
+    const int lane = threadIdx.x & 31;
+    const int st = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
+    if (st >= n_sub) return;
+    const size_t f = blockIdx.y;
+    const float* d = depth + f * WH;
+    const int32_t* l = labels + f * WH;
+    int32_t* h = hist + f * (size_t)R * n_sub;
+    const size_t beg = (size_t)st * sub_tile;
+    const size_t end = min(beg + (size_t)sub_tile, (size_t)WH);
+    int cur = -1, cnt = 0;
+    for (size_t i0 = beg; i0 < end; i0 += 32) {
+        const int lab = pixel_label(d, l, i0 + lane, end, R);
+        if (__all_sync(kFull, lab == cur || lab < 0)) {
+            cnt += __popc(__ballot_sync(kFull, lab >= 0));
+            continue;
+        }
+        const int L = __reduce_max_sync(kFull, lab);
+        if (cur >= 0 && lane == 0) h[(size_t)cur * n_sub + st] += cnt;
+        __syncwarp();
+        if (__all_sync(kFull, lab == L || lab < 0)) {          // one new label
+            cur = L;
+            cnt = __popc(__ballot_sync(kFull, lab >= 0));
+            continue;
+        }
+        cur = -1;                                              // mixed step
+        cnt = 0;
+        const unsigned m = __match_any_sync(kFull, lab);
+        if (lab >= 0 && lane == __ffs(m) - 1) h[(size_t)lab * n_sub + st] += __popc(m);
+        __syncwarp();
+    }
+    if (cur >= 0 && lane == 0) h[(size_t)cur * n_sub + st] += cnt;
+}
+
+// one warp per (frame, region): exclusive prefix over sub-tiles, total count
+__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+compact_scan_kernel(int R, int n_sub, int32_t* __restrict__ hist, int32_t* __restrict__ region_cnt) {
+    const int lane = threadIdx.x & 31;
+    const int r = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
+    if (r >= R) return;
+    const size_t f = blockIdx.y;
+    int32_t* row = hist + (f * R + r) * (size_t)n_sub;
+    int carry = 0;
+    for (int s0 = 0; s0 < n_sub; s0 += 32) {
+        const int s = s0 + lane;
+        const int v = s < n_sub ? row[s] : 0;
+        int incl = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(kFull, incl, o);
+            if (lane >= o) incl += t;
+        }
+        if (s < n_sub) row[s] = carry + incl - v;
+        carry += __shfl_sync(kFull, incl, 31);
+    }
+    if (lane == 0) region_cnt[f * R + r] = carry;
+}
+
+// one block per frame: region_off[f][0..R] = exclusive prefix of region_cnt
+__global__ void __launch_bounds__(1024)
+compact_offsets_kernel(int R, const int32_t* __restrict__ region_cnt, int32_t* __restrict__ region_off) {
+    __shared__ int warp_tot[32];
+    __shared__ int carry_s;
+    const size_t f = blockIdx.x;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int32_t* cnt = region_cnt + f * R;
+    int32_t* off = region_off + f * (size_t)(R + 1);
+    if (threadIdx.x == 0) carry_s = 0;
+    __syncthreads();
+    for (int base = 0; base < R; base += 1024) {
+        const int r = base + threadIdx.x;
+        const int v = r < R ? cnt[r] : 0;
+        int incl = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(kFull, incl, o);
+            if (lane >= o) incl += t;
+        }
+        if (lane == 31) warp_tot[w] = incl;
+        __syncthreads();
+        if (w == 0) {
+            int x = warp_tot[lane];
+            int xi = x;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int t = __shfl_up_sync(kFull, xi, o);
+                if (lane >= o) xi += t;
+            }
+            warp_tot[lane] = xi - x;                         // exclusive warp prefix
+        }
+        __syncthreads();
+        const int carry = carry_s;
+        if (r < R) off[r] = carry + warp_tot[w] + incl - v;
+        __syncthreads();
+        if (threadIdx.x == 1023) carry_s = carry + warp_tot[w] + incl;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) off[R] = carry_s;
+}
+
+__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+compact_scatter_kernel(const float* __restrict__ depth, const int32_t* __restrict__ labels,
+                       int W, int WH, int R, int sub_tile, int n_sub, int32_t* __restrict__ hist,
+                       const int32_t* __restrict__ region_off, uint2* __restrict__ points) {
+    const int lane = threadIdx.x & 31;
+    const int st = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
+    if (st >= n_sub) return;
+    const size_t f = blockIdx.y;
+    const float* d = depth + f * WH;
+    const int32_t* l = labels + f * WH;
+    int32_t* h = hist + f * (size_t)R * n_sub;
+    const int32_t* off = region_off + f * (size_t)(R + 1);
+    uint2* pts = points + f * WH;
+    const size_t beg = (size_t)st * sub_tile;
+    const size_t end = min(beg + (size_t)sub_tile, (size_t)WH);
+    const unsigned lt = lanemask_lt();
+    int cur = -1, rel = 0, roff = 0;       // cached label, next rank within region, region offset
+    for (size_t i0 = beg; i0 < end; i0 += 32) {
+        const size_t i = i0 + lane;
+        const int lab = pixel_label(d, l, i, end, R);
+        uint2 pk = make_uint2(0u, 0u);
+        if (lab >= 0) {
+            const unsigned u = (unsigned)(i % (unsigned)W), v = (unsigned)(i / (unsigned)W);
+            pk = make_uint2(u | (v << 16), __float_as_uint(__ldg(d + i)));
+        }
+        bool fast = __all_sync(kFull, lab == cur || lab < 0);
+        if (!fast) {
+            const int L = __reduce_max_sync(kFull, lab);
+            if (cur >= 0 && lane == 0) h[(size_t)cur * n_sub + st] = rel;     // flush
+            __syncwarp();
+            if (__all_sync(kFull, lab == L || lab < 0)) {
+                cur = L;
+                rel = h[(size_t)L * n_sub + st];
+                roff = off[L];
+                fast = true;
+            } else {
+                cur = -1;
+                const unsigned m = __match_any_sync(kFull, lab);
+                const int leader = __ffs(m) - 1;
+                int b = 0;
+                if (lab >= 0 && lane == leader) {
+                    const int r0 = h[(size_t)lab * n_sub + st];
+                    h[(size_t)lab * n_sub + st] = r0 + __popc(m);
+                    b = off[lab] + r0;
+                }
+                b = __shfl_sync(kFull, b, leader);
+                if (lab >= 0) pts[b + __popc(m & lt)] = pk;
+                __syncwarp();
+            }
+        }
+        if (fast) {
+            const unsigned bal = __ballot_sync(kFull, lab >= 0);
+            if (lab >= 0) pts[roff + rel + __popc(bal & lt)] = pk;
+            rel += __popc(bal);
+        }
+    }
+    if (cur >= 0 && lane == 0) h[(size_t)cur * n_sub + st] = rel;
+}
+
+}  // namespace
+
+cudaError_t compact_run(const float* depth, const int32_t* labels, const RansacWorkspace& ws,
+                        cudaStream_t stream) {
+    const int WH = ws.W * ws.H;
+    cudaError_t e = cudaMemsetAsync(ws.hist, 0, sizeof(int32_t) * (size_t)ws.B * ws.R * ws.n_sub, stream);
+    if (e != cudaSuccess) return e;
+    const dim3 blk(kWarpsPerBlock * 32);
+    const dim3 g_tiles((ws.n_sub + kWarpsPerBlock - 1) / kWarpsPerBlock, ws.B);
+    compact_count_kernel<<<g_tiles, blk, 0, stream>>>(depth, labels, WH, ws.R, ws.sub_tile, ws.n_sub, ws.hist);
+    const dim3 g_regions((ws.R + kWarpsPerBlock - 1) / kWarpsPerBlock, ws.B);
+    compact_scan_kernel<<<g_regions, blk, 0, stream>>>(ws.R, ws.n_sub, ws.hist, ws.region_cnt);
+    compact_offsets_kernel<<<ws.B, 1024, 0, stream>>>(ws.R, ws.region_cnt, ws.region_off);
+    compact_scatter_kernel<<<g_tiles, blk, 0, stream>>>(depth, labels, ws.W, WH, ws.R, ws.sub_tile,
+                                                        ws.n_sub, ws.hist, ws.region_off, ws.points);
+    return cudaGetLastError();
+}
+
+}  // namespace pm

@@ -1,0 +1,54 @@
+// internal.h — launch functions behind the C ABI (not exported).
+#pragma once
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+#include "../../include/pmap.h"
+
+namespace pm {
+
+// ---- adf.cu
+cudaError_t adf_setup_attributes();
+int adf_default_iters_per_pass();
+// in -> out (B frames); ws: B*H*W floats (used when >= 2 passes); normals nullable.
+cudaError_t adf_run(const float* in, float* out, float* normals, float* ws, int W, int H, int B,
+                    const pm_intrinsics* K, float lam, float kappa, int iters, int iters_per_pass,
+                    cudaStream_t stream);
+cudaError_t normals_run(const float* depth, float* normals, int W, int H, int B,
+                        const pm_intrinsics* K, cudaStream_t stream);
+
+// ---- compact.cu / ransac.cu
+struct RansacWorkspace {
+    // sizes
+    int W, H, B, R, n_hyp, n_hyp_pad, sub_tile, n_sub;
+    // buffers (device)
+    uint2* points;        // [B][W*H] packed (u | v<<16, z bits), region-major, raster order
+    int32_t* hist;        // [B][R][n_sub] count -> exclusive prefix per region
+    int32_t* region_cnt;  // [B][R]
+    int32_t* region_off;  // [B][R+1]
+    float4* planes;       // [B][R][n_hyp_pad] hypothesis planes (NaN = invalid)
+    int32_t* counts;      // [B][R][n_hyp_pad] inlier counts (-1 = invalid)
+    uint64_t* errq;       // [B][R][n_hyp_pad] fixed-point error sums (select=ERROR / debug)
+    size_t total_bytes;
+};
+// Carve `base` (nullable: sizing only) into the ransac workspace.
+RansacWorkspace ransac_workspace_layout(void* base, int W, int H, int R, int n_hyp, int B);
+
+cudaError_t compact_run(const float* depth, const int32_t* labels, const RansacWorkspace& ws,
+                        cudaStream_t stream);
+
+struct RansacArgs {
+    pm_intrinsics K;
+    float tau;
+    uint64_t seed;
+    uint32_t first_frame;
+    int sampler;
+    int select;
+    int32_t* counts_out;   // nullable debug
+    uint64_t* errq_out;    // nullable debug
+};
+cudaError_t ransac_run(const RansacWorkspace& ws, const RansacArgs& a, pm_plane* planes,
+                       cudaStream_t stream);
+
+}  // namespace pm

@@ -1,0 +1,424 @@
+// ransac.cu — Algorithm 2 of arXiv 2411.01919, batched over every
+// region of every frame in three launches:
+//   hyp    : one thread per (frame, region, hypothesis): Philox sample ->
+//            3 points -> f32 plane (Alg. 2 ℓ6-7)
+//   score  : the hot loop (ℓ9-13).  The compacted points of a frame are cut
+//            into fixed chunks, one CTA per chunk regardless of region sizes
+//            (load balance); a chunk's points are deprojected once into
+//            shared memory and scored against every hypothesis of the
+//            region(s) it overlaps, 8 hypotheses per register block; counts
+//            are warp-reduced (REDUX) and added to global integer counters
+//            (exact, order-free)
+//   select : one CTA per (frame, region): argmax count (ties -> lowest h,
+//            ℓ14-17), fp64 least-squares refit over the winner's inliers, gate
+//            (ℓ19), pm_plane output.
+// All plane and distance arithmetic uses explicit _rn intrinsics in the f32
+// order DESIGN.md §3 fixes, so counts are bit-identical to the oracle's.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "common.cuh"
+#include "internal.h"
+
+namespace pm {
+
+namespace {
+
+constexpr unsigned kFull = 0xFFFFFFFFu;
+constexpr int kScoreThreads = 256;
+constexpr int kChunk = 2048;          // points per scoring CTA
+constexpr int kHB = 8;                // hypotheses per register block
+constexpr int kSelectThreads = 256;
+
+struct SampleIdx { uint32_t i0, i1, i2; bool ok; };
+
+// Alg. 2 ℓ6 (Q17): three distinct uniform indices in [0, n) from Philox draws.
+PM_DEVINL SampleIdx sample_philox(uint32_t h, uint32_t r, uint32_t f, uint64_t seed, uint32_t n) {
+    const U4 x = philox4x32_10(U4{h, r, f, 0u}, (uint32_t)seed, (uint32_t)(seed >> 32));
+    uint32_t i0 = __umulhi(x.x, n);
+    uint32_t i1 = __umulhi(x.y, n - 1);
+    if (i1 >= i0) i1++;
+    const uint32_t a = min(i0, i1), b = max(i0, i1);
+    uint32_t i2 = __umulhi(x.z, n - 2);
+    if (i2 >= a) i2++;
+    if (i2 >= b) i2++;
+    return SampleIdx{i0, i1, i2, true};
+}
+
+// Test sampler ENUMERATE: h -> h-th 3-combination of [0, n) in colex order.
+PM_DEVINL uint64_t binom3(uint64_t m) { return m < 3 ? 0 : m * (m - 1) * (m - 2) / 6; }
+PM_DEVINL uint64_t binom2(uint64_t m) { return m < 2 ? 0 : m * (m - 1) / 2; }
+PM_DEVINL SampleIdx sample_colex(uint32_t h, uint32_t n) {
+    uint64_t hh = h;
+    uint32_t c2 = 2;
+    while (binom3(c2 + 1) <= hh) c2++;
+    hh -= binom3(c2);
+    uint32_t c1 = 1;
+    while (binom2(c1 + 1) <= hh) c1++;
+    hh -= binom2(c1);
+    return SampleIdx{(uint32_t)hh, c1, c2, c2 < n};
+}
+
+PM_DEVINL SampleIdx sample(int sampler, uint32_t h, uint32_t r, uint32_t f, uint64_t seed, uint32_t n) {
+    return sampler == PM_SAMPLER_ENUMERATE ? sample_colex(h, n) : sample_philox(h, r, f, seed, n);
+}
+
+// Alg. 2 ℓ7: plane through three points, f32 in the fixed order; d >= 0.
+// Returns false for a collinear sample: !(|e1 x e2|^2 > 1e-12 |e1|^2 |e2|^2).
+PM_DEVINL bool plane_from_3pts(float3 p0, float3 p1, float3 p2, float4& pl) {
+    const float e1x = __fsub_rn(p1.x, p0.x), e1y = __fsub_rn(p1.y, p0.y), e1z = __fsub_rn(p1.z, p0.z);
+    const float e2x = __fsub_rn(p2.x, p0.x), e2y = __fsub_rn(p2.y, p0.y), e2z = __fsub_rn(p2.z, p0.z);
+    const float cx = __fsub_rn(__fmul_rn(e1y, e2z), __fmul_rn(e1z, e2y));
+    const float cy = __fsub_rn(__fmul_rn(e1z, e2x), __fmul_rn(e1x, e2z));
+    const float cz = __fsub_rn(__fmul_rn(e1x, e2y), __fmul_rn(e1y, e2x));
+    const float s2 = __fadd_rn(__fadd_rn(__fmul_rn(cx, cx), __fmul_rn(cy, cy)), __fmul_rn(cz, cz));
+    const float l1 = __fadd_rn(__fadd_rn(__fmul_rn(e1x, e1x), __fmul_rn(e1y, e1y)), __fmul_rn(e1z, e1z));
+    const float l2 = __fadd_rn(__fadd_rn(__fmul_rn(e2x, e2x), __fmul_rn(e2y, e2y)), __fmul_rn(e2z, e2z));
+    if (!(s2 > __fmul_rn(1e-12f, __fmul_rn(l1, l2)))) return false;
+    const float len = __fsqrt_rn(s2);
+    float nx = __fdiv_rn(cx, len), ny = __fdiv_rn(cy, len), nz = __fdiv_rn(cz, len);
+    float d = -__fadd_rn(__fadd_rn(__fmul_rn(nx, p0.x), __fmul_rn(ny, p0.y)), __fmul_rn(nz, p0.z));
+    if (d < 0.0f) { nx = -nx; ny = -ny; nz = -nz; d = -d; }
+    pl = make_float4(nx, ny, nz, d);
+    return true;
+}
+
+__global__ void __launch_bounds__(256)
+ransac_hyp_kernel(RansacWorkspace ws, RansacArgs a, int need_err) {
+    const int idx = blockIdx.x * 256 + threadIdx.x;
+    const int R = ws.R, HP = ws.n_hyp_pad;
+    if (idx >= R * HP) return;
+    const int r = idx / HP, h = idx % HP;
+    const size_t f = blockIdx.y;
+    const size_t slot = (f * R + r) * HP + h;
+    const int32_t* off = ws.region_off + f * (size_t)(R + 1);
+    const uint32_t n = (uint32_t)(off[r + 1] - off[r]);
+    float4 pl = make_float4(__int_as_float(0x7FC00000), 0.f, 0.f, 0.f);   // NaN = invalid
+    int c0 = -1;
+    if (h < ws.n_hyp && n >= 3) {
+        const SampleIdx s = sample(a.sampler, (uint32_t)h, (uint32_t)r, a.first_frame + (uint32_t)f, a.seed, n);
+        if (s.ok) {
+            const uint2* pts = ws.points + f * (size_t)ws.W * ws.H + off[r];
+            const float ifx = 1.0f / a.K.fx, ify = 1.0f / a.K.fy;   // host-identical IEEE division
+            const uint2 q0 = pts[s.i0], q1 = pts[s.i1], q2 = pts[s.i2];
+            const float3 p0 = deproject(PackedPoint{q0.x, __uint_as_float(q0.y)}, a.K.cx, a.K.cy, ifx, ify);
+            const float3 p1 = deproject(PackedPoint{q1.x, __uint_as_float(q1.y)}, a.K.cx, a.K.cy, ifx, ify);
+            const float3 p2 = deproject(PackedPoint{q2.x, __uint_as_float(q2.y)}, a.K.cx, a.K.cy, ifx, ify);
+            float4 t;
+            if (plane_from_3pts(p0, p1, p2, t)) { pl = t; c0 = 0; }
+        }
+    }
+    ws.planes[slot] = pl;
+    ws.counts[slot] = c0;
+    if (need_err) ws.errq[slot] = 0ull;
+}
+
+// The hot loop.  grid = (ceil(W*H / kChunk), B).
+template <bool WITH_ERR>
+__global__ void __launch_bounds__(kScoreThreads)
+ransac_score_kernel(RansacWorkspace ws, RansacArgs a) {
+    __shared__ float4 sp[kChunk];
+    __shared__ int s_r0;
+    const size_t f = blockIdx.y;
+    const int R = ws.R, HP = ws.n_hyp_pad;
+    const int32_t* off = ws.region_off + f * (size_t)(R + 1);
+    const int total = off[R];
+    const int s = blockIdx.x * kChunk;
+    if (s >= total) return;
+    const int e = min(s + kChunk, total);
+    const uint2* pts = ws.points + f * (size_t)ws.W * ws.H;
+    const float ifx = 1.0f / a.K.fx, ify = 1.0f / a.K.fy;
+    for (int i = threadIdx.x; i < e - s; i += kScoreThreads) {
+        const uint2 q = pts[s + i];
+        const float3 P = deproject(PackedPoint{q.x, __uint_as_float(q.y)}, a.K.cx, a.K.cy, ifx, ify);
+        sp[i] = make_float4(P.x, P.y, P.z, 0.f);
+    }
+    if (threadIdx.x == 0) {                 // first region with off[r] <= s < off[r+1]
+        int lo = 0, hi = R;                 // invariant: off[lo] <= s, off[hi] = total > s
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (off[mid] <= s) lo = mid; else hi = mid;
+        }
+        s_r0 = lo;
+    }
+    __syncthreads();
+    const float tau = a.tau;
+    const int lane = threadIdx.x & 31;
+    for (int r = s_r0; r < R && off[r] < e; ++r) {
+        const int lo = max(s, off[r]) - s, hi = min(e, off[r + 1]) - s;
+        if (hi <= lo) continue;
+        const float4* planes = ws.planes + (f * R + r) * HP;
+        int32_t* counts = ws.counts + (f * R + r) * HP;
+        uint64_t* errq = ws.errq + (f * R + r) * HP;
+        for (int h0 = 0; h0 < ws.n_hyp; h0 += kHB) {
+            float4 pl[kHB];
+#pragma unroll
+            for (int j = 0; j < kHB; ++j) pl[j] = __ldg(planes + h0 + j);
+            int c[kHB];
+            uint64_t eq[kHB];
+#pragma unroll
+            for (int j = 0; j < kHB; ++j) { c[j] = 0; eq[j] = 0; }
+            for (int i = lo + threadIdx.x; i < hi; i += kScoreThreads) {
+                const float4 p4 = sp[i];
+                const float3 P = make_float3(p4.x, p4.y, p4.z);
+#pragma unroll
+                for (int j = 0; j < kHB; ++j) {
+                    const float dist = plane_dist(pl[j], P);
+                    c[j] += dist < tau ? 1 : 0;
+                    if (WITH_ERR) eq[j] += __float2ull_rn(__fmul_rn(fminf(dist, 64.0f), 16777216.0f));
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < kHB; ++j) {
+                const int cw = __reduce_add_sync(kFull, c[j]);
+                if (lane == 0 && cw > 0) atomicAdd(counts + h0 + j, cw);
+                if (WITH_ERR) {
+                    uint64_t ew = eq[j];
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) ew += __shfl_xor_sync(kFull, ew, o);
+                    if (lane == 0 && ew > 0 && !isnan(pl[j].x))
+                        atomicAdd((unsigned long long*)(errq + h0 + j), (unsigned long long)ew);
+                }
+            }
+        }
+    }
+}
+
+// ---- fp64 refit helpers
+struct Sums {
+    double s[3];     // sum of q = p - o over inliers
+    double m[6];     // sum of q q^T (xx, xy, xz, yy, yz, zz)
+    int n;
+    unsigned long long err;
+};
+
+PM_DEVINL void sums_add(Sums& a, const Sums& b) {
+#pragma unroll
+    for (int k = 0; k < 3; ++k) a.s[k] += b.s[k];
+#pragma unroll
+    for (int k = 0; k < 6; ++k) a.m[k] += b.m[k];
+    a.n += b.n;
+    a.err += b.err;
+}
+
+PM_DEVINL Sums sums_shfl_xor(const Sums& a, int o) {
+    Sums b;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) b.s[k] = __shfl_xor_sync(kFull, a.s[k], o);
+#pragma unroll
+    for (int k = 0; k < 6; ++k) b.m[k] = __shfl_xor_sync(kFull, a.m[k], o);
+    b.n = __shfl_xor_sync(kFull, a.n, o);
+    b.err = __shfl_xor_sync(kFull, a.err, o);
+    return b;
+}
+
+// Smallest-eigenvalue eigenvector of a symmetric 3x3 (double) by cyclic
+// Jacobi rotations (Golub & Van Loan, symmetric Schur decomposition).
+PM_DEVINL void smallest_eigvec(double A[3][3], double out[3]) {
+    double V[3][3] = {{1, 0, 0}, {0, 1, 0}, {0, 0, 1}};
+    const double scale = fabs(A[0][0]) + fabs(A[1][1]) + fabs(A[2][2]);
+    for (int sweep = 0; sweep < 64; ++sweep) {
+        const double off = sqrt(A[0][1] * A[0][1] + A[0][2] * A[0][2] + A[1][2] * A[1][2]);
+        if (off == 0.0 || off <= 1e-15 * scale) break;
+        for (int k = 0; k < 3; ++k) {
+            const int p = k == 2 ? 1 : 0, q = k == 0 ? 1 : 2;
+            const double apq = A[p][q];
+            if (apq == 0.0) continue;
+            const double tau = (A[q][q] - A[p][p]) / (2.0 * apq);
+            const double t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
+            const double c = rsqrt(1.0 + t * t), sn = t * c;
+            for (int i = 0; i < 3; ++i) {            // A <- A J
+                const double aip = A[i][p], aiq = A[i][q];
+                A[i][p] = c * aip - sn * aiq;
+                A[i][q] = sn * aip + c * aiq;
+            }
+            for (int i = 0; i < 3; ++i) {            // A <- J^T A
+                const double api = A[p][i], aqi = A[q][i];
+                A[p][i] = c * api - sn * aqi;
+                A[q][i] = sn * api + c * aqi;
+            }
+            for (int i = 0; i < 3; ++i) {            // V <- V J
+                const double vip = V[i][p], viq = V[i][q];
+                V[i][p] = c * vip - sn * viq;
+                V[i][q] = sn * vip + c * viq;
+            }
+        }
+    }
+    int m = 0;
+    if (A[1][1] < A[m][m]) m = 1;
+    if (A[2][2] < A[m][m]) m = 2;
+    const double nn = sqrt(V[0][m] * V[0][m] + V[1][m] * V[1][m] + V[2][m] * V[2][m]);
+    out[0] = V[0][m] / nn;
+    out[1] = V[1][m] / nn;
+    out[2] = V[2][m] / nn;
+}
+
+__global__ void __launch_bounds__(kSelectThreads)
+ransac_select_kernel(RansacWorkspace ws, RansacArgs a, pm_plane* __restrict__ planes_out) {
+    __shared__ unsigned long long s_key[kSelectThreads / 32];
+    __shared__ int s_h[kSelectThreads / 32];
+    __shared__ Sums s_sums[kSelectThreads / 32];
+    const int r = blockIdx.x;
+    const size_t f = blockIdx.y;
+    const int R = ws.R, HP = ws.n_hyp_pad, NH = ws.n_hyp;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int32_t* off = ws.region_off + f * (size_t)(R + 1);
+    const int base = off[r];
+    const int n = off[r + 1] - base;
+    const int32_t* counts = ws.counts + (f * R + r) * HP;
+    const uint64_t* errq = ws.errq + (f * R + r) * HP;
+    pm_plane* out = planes_out + f * R + r;
+    if (a.counts_out)
+        for (int h = threadIdx.x; h < NH; h += kSelectThreads) a.counts_out[(f * R + r) * NH + h] = counts[h];
+    if (a.errq_out)
+        for (int h = threadIdx.x; h < NH; h += kSelectThreads) a.errq_out[(f * R + r) * NH + h] = errq[h];
+
+    pm_plane res;
+    for (int k = 0; k < 3; ++k) { res.n[k] = 0.f; res.centroid[k] = 0.f; }
+    res.d = 0.f; res.inliers = 0; res.n_points = n; res.best_hyp = -1; res.sum_dist = 0.f;
+    if (n < 3) {
+        res.status = PM_PLANE_TOO_FEW;
+        if (threadIdx.x == 0) *out = res;
+        return;
+    }
+    // ---- ℓ14-17: selection.  score orders "better" hypotheses higher (0 =
+    // invalid): count + 1 (argmax inliers), or ~errq (argmin error, as printed);
+    // ties go to the lowest h.
+    unsigned long long best_p = 0ull;
+    int best_h = 0x7FFFFFFF;
+    for (int h = threadIdx.x; h < NH; h += kSelectThreads) {
+        const int c = counts[h];
+        if (c < 0) continue;
+        const unsigned long long sc = a.select == PM_SELECT_ERROR ? ~(unsigned long long)errq[h]
+                                                                  : (unsigned long long)(c + 1);
+        if (sc > best_p || (sc == best_p && h < best_h)) { best_p = sc; best_h = h; }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long op = __shfl_xor_sync(kFull, best_p, o);
+        const int oh = __shfl_xor_sync(kFull, best_h, o);
+        if (op > best_p || (op == best_p && oh < best_h)) { best_p = op; best_h = oh; }
+    }
+    if (lane == 0) { s_key[w] = best_p; s_h[w] = best_h; }
+    __syncthreads();
+    best_p = s_key[0];
+    best_h = s_h[0];
+    for (int k = 1; k < kSelectThreads / 32; ++k)
+        if (s_key[k] > best_p || (s_key[k] == best_p && s_h[k] < best_h)) { best_p = s_key[k]; best_h = s_h[k]; }
+    if (best_p == 0ull) {
+        res.status = PM_PLANE_DEGENERATE;
+        if (threadIdx.x == 0) *out = res;
+        return;
+    }
+    const int best = best_h;
+    const float4 pl = ws.planes[(f * R + r) * HP + best];
+    const uint2* pts = ws.points + f * (size_t)ws.W * ws.H + base;
+    const float ifx = 1.0f / a.K.fx, ify = 1.0f / a.K.fy;
+
+    // ---- refit: shifted fp64 moments of the winner's inliers (one pass)
+    const uint2 q0 = pts[0];
+    const float3 o3 = deproject(PackedPoint{q0.x, __uint_as_float(q0.y)}, a.K.cx, a.K.cy, ifx, ify);
+    const double ox = o3.x, oy = o3.y, oz = o3.z;
+    Sums acc = {};
+    for (int i = threadIdx.x; i < n; i += kSelectThreads) {
+        const uint2 q = pts[i];
+        const float3 P = deproject(PackedPoint{q.x, __uint_as_float(q.y)}, a.K.cx, a.K.cy, ifx, ify);
+        const float dist = plane_dist(pl, P);
+        acc.err += __float2ull_rn(__fmul_rn(fminf(dist, 64.0f), 16777216.0f));
+        if (dist < a.tau) {
+            const double x = (double)P.x - ox, y = (double)P.y - oy, z = (double)P.z - oz;
+            acc.s[0] += x; acc.s[1] += y; acc.s[2] += z;
+            acc.m[0] += x * x; acc.m[1] += x * y; acc.m[2] += x * z;
+            acc.m[3] += y * y; acc.m[4] += y * z; acc.m[5] += z * z;
+            acc.n += 1;
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sums_add(acc, sums_shfl_xor(acc, o));
+    if (lane == 0) s_sums[w] = acc;
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    Sums t = s_sums[0];
+    for (int k = 1; k < kSelectThreads / 32; ++k) sums_add(t, s_sums[k]);
+
+    const int inl = counts[best];
+    double nv[3], cen[3], dd;
+    if (t.n >= 3) {
+        const double inv = 1.0 / t.n;
+        const double mx = t.s[0] * inv, my = t.s[1] * inv, mz = t.s[2] * inv;
+        double A[3][3];
+        A[0][0] = t.m[0] - t.n * mx * mx; A[0][1] = t.m[1] - t.n * mx * my; A[0][2] = t.m[2] - t.n * mx * mz;
+        A[1][1] = t.m[3] - t.n * my * my; A[1][2] = t.m[4] - t.n * my * mz; A[2][2] = t.m[5] - t.n * mz * mz;
+        A[1][0] = A[0][1]; A[2][0] = A[0][2]; A[2][1] = A[1][2];
+        smallest_eigvec(A, nv);
+        cen[0] = ox + mx; cen[1] = oy + my; cen[2] = oz + mz;
+    } else {
+        // refit impossible (tau below rounding): keep the 3-point model,
+        // centroid = mean of its three sample points (Q19)
+        const SampleIdx s = sample(a.sampler, (uint32_t)best, (uint32_t)r, a.first_frame + (uint32_t)f, a.seed, (uint32_t)n);
+        const uint32_t id[3] = {s.i0, s.i1, s.i2};
+        cen[0] = cen[1] = cen[2] = 0.0;
+        for (int k = 0; k < 3; ++k) {
+            const uint2 q = pts[id[k]];
+            const float3 P = deproject(PackedPoint{q.x, __uint_as_float(q.y)}, a.K.cx, a.K.cy, ifx, ify);
+            cen[0] += P.x; cen[1] += P.y; cen[2] += P.z;
+        }
+        for (int k = 0; k < 3; ++k) cen[k] /= 3.0;
+        nv[0] = pl.x; nv[1] = pl.y; nv[2] = pl.z;
+    }
+    dd = -(nv[0] * cen[0] + nv[1] * cen[1] + nv[2] * cen[2]);
+    if (t.n < 3) dd = pl.w;
+    if (dd < 0.0) { nv[0] = -nv[0]; nv[1] = -nv[1]; nv[2] = -nv[2]; dd = -dd; }
+    for (int k = 0; k < 3; ++k) { res.n[k] = (float)nv[k]; res.centroid[k] = (float)cen[k]; }
+    res.d = (float)dd;
+    res.inliers = inl;
+    res.best_hyp = best;
+    res.status = (10ll * inl > 9ll * n) ? PM_PLANE_OK : PM_PLANE_REJECTED;   // ℓ19
+    res.sum_dist = (float)((double)t.err * (1.0 / 16777216.0));
+    *out = res;
+}
+
+}  // namespace
+
+static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+RansacWorkspace ransac_workspace_layout(void* base, int W, int H, int R, int n_hyp, int B) {
+    RansacWorkspace ws{};
+    ws.W = W; ws.H = H; ws.B = B; ws.R = R; ws.n_hyp = n_hyp;
+    ws.n_hyp_pad = ((n_hyp + kHB - 1) / kHB) * kHB;
+    const size_t WH = (size_t)W * H;
+    int st = 1024;
+    while (st < 4 * R && st < (1 << 24)) st <<= 1;      // hist entries <= ~W*H/4 per frame
+    ws.sub_tile = st;
+    ws.n_sub = (int)((WH + st - 1) / st);
+    const size_t Rm = R > 0 ? R : 1;
+    size_t o = 0;
+    char* p = (char*)base;
+    auto take = [&](size_t bytes) { char* q = p ? p + o : nullptr; o += align256(bytes); return (void*)q; };
+    ws.points = (uint2*)take(sizeof(uint2) * B * WH);
+    ws.hist = (int32_t*)take(sizeof(int32_t) * B * Rm * ws.n_sub);
+    ws.region_cnt = (int32_t*)take(sizeof(int32_t) * B * Rm);
+    ws.region_off = (int32_t*)take(sizeof(int32_t) * B * (Rm + 1));
+    ws.planes = (float4*)take(sizeof(float4) * B * Rm * ws.n_hyp_pad);
+    ws.counts = (int32_t*)take(sizeof(int32_t) * B * Rm * ws.n_hyp_pad);
+    ws.errq = (uint64_t*)take(sizeof(uint64_t) * B * Rm * ws.n_hyp_pad);
+    ws.total_bytes = o;
+    return ws;
+}
+
+cudaError_t ransac_run(const RansacWorkspace& ws, const RansacArgs& a, pm_plane* planes,
+                       cudaStream_t stream) {
+    const bool need_err = a.select == PM_SELECT_ERROR || a.errq_out != nullptr;
+    const int n_hyp_slots = ws.R * ws.n_hyp_pad;
+    ransac_hyp_kernel<<<dim3((n_hyp_slots + 255) / 256, ws.B), 256, 0, stream>>>(ws, a, need_err ? 1 : 0);
+    const dim3 g_score((unsigned)(((size_t)ws.W * ws.H + kChunk - 1) / kChunk), ws.B);
+    if (need_err)
+        ransac_score_kernel<true><<<g_score, kScoreThreads, 0, stream>>>(ws, a);
+    else
+        ransac_score_kernel<false><<<g_score, kScoreThreads, 0, stream>>>(ws, a);
+    ransac_select_kernel<<<dim3(ws.R, ws.B), kSelectThreads, 0, stream>>>(ws, a, planes);
+    return cudaGetLastError();
+}
+
+}  // namespace pm

@@ -1,0 +1,216 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle, element
+by element, on the same seeded inputs (DESIGN.md §6 test matrix).
+
+Tolerances (north_star / DESIGN.md §6): ADF depth |d| <= 1e-4 m on valid
+pixels, invalid pixels bitwise; normals angle <= 1e-3 rad with the invalid
+mask bitwise; RANSAC per-hypothesis counts, selected index, n_points and
+status bit-exact; refit n, d, centroid within 1e-5."""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import scenegen
+
+pytestmark = pytest.mark.gpu
+
+ADF_TOL = 1e-4
+ANG_TOL = 1e-3
+REFIT_TOL = 1e-5
+
+
+@pytest.fixture(scope="module")
+def pm():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2411_01919_b200 as pm
+    return pm
+
+
+DEV = "cuda"
+
+
+def _angle(a, b):
+    c = np.cross(a, b, axis=0)
+    return np.arctan2(np.linalg.norm(c, axis=0), (a * b).sum(0))
+
+
+def _check_normals(n_gpu, n_ref):
+    n_gpu = n_gpu.astype(np.float64)
+    zg = np.all(n_gpu == 0, axis=0)
+    zr = np.all(n_ref == 0, axis=0)
+    assert np.array_equal(zg, zr), f"invalid masks differ at {np.argwhere(zg != zr)[:5]}"
+    ang = _angle(n_gpu[:, ~zr], n_ref[:, ~zr])
+    assert ang.size == 0 or ang.max() <= ANG_TOL, ang.max()
+    if ang.size:
+        assert np.abs(np.linalg.norm(n_gpu[:, ~zr], axis=0) - 1).max() < 1e-5
+    return float(ang.max()) if ang.size else 0.0
+
+
+def _check_depth(d_gpu, d_in, d_ref):
+    valid = (d_in > 0) & np.isfinite(d_in)
+    assert d_gpu[~valid].tobytes() == d_in[~valid].tobytes(), "invalid pixels must be copied bitwise"
+    err = np.abs(d_gpu[valid].astype(np.float64) - d_ref[valid].astype(np.float64))
+    assert err.size == 0 or err.max() <= ADF_TOL, err.max()
+    return float(err.max()) if err.size else 0.0
+
+
+FRAMES = [
+    ("C1", {}), ("C1n", {}), ("C1n", {"holes": 0.02}), ("C2", {}), ("C2", {"holes": 0.01}),
+    ("C2", {"W": 333, "H": 251}), ("RAMP", {}),
+]
+
+
+@pytest.mark.parametrize("name,kw", FRAMES)
+def test_adf_and_fused_normals(pm, name, kw):
+    fr = scenegen.make_config(name, **kw)
+    iters = fr["iters"] if name != "RAMP" else 7
+    d_in = fr["depth"].numpy()
+    d_out, nrm = pm.adf_filter(fr["depth"].to(DEV), fr["K"], fr["lam"], fr["kappa"], iters)
+    torch.cuda.synchronize()
+    d_gpu = d_out.cpu().numpy()
+    _check_depth(d_gpu, d_in, oracle.adf(d_in, fr["lam"], fr["kappa"], iters))
+    # fused normals against the oracle's normals of the GPU's own filtered depth
+    _check_normals(nrm.cpu().numpy(), oracle.normals(d_gpu, fr["K"]))
+
+
+@pytest.mark.parametrize("name,kw", FRAMES)
+def test_normals_standalone(pm, name, kw):
+    fr = scenegen.make_config(name, **kw)
+    n = pm.normals_from_depth(fr["depth"].to(DEV), fr["K"])
+    torch.cuda.synchronize()
+    _check_normals(n.cpu().numpy(), oracle.normals(fr["depth"].numpy(), fr["K"]))
+
+
+def test_adf_special_values_and_edges(pm):
+    # NaN / inf / negative / zero pixels copied bitwise; N = 0 copies the
+    # input; a constant image is a bitwise fixed point (P4)
+    rng = np.random.default_rng(0)
+    d = (1.0 + 0.01 * rng.standard_normal((37, 45))).astype(np.float32)
+    d[3, 4], d[10, 10], d[20, 0], d[36, 44], d[0, 0] = np.nan, np.inf, -2.0, 0.0, -0.0
+    K = scenegen.intrinsics_for(45, 37)
+    for it in (0, 1, 5, 13):
+        out, nrm = pm.adf_filter(torch.from_numpy(d).to(DEV), K, 0.2, 0.02, it)
+        torch.cuda.synchronize()
+        _check_depth(out.cpu().numpy(), d, oracle.adf(d, 0.2, 0.02, it))
+        _check_normals(nrm.cpu().numpy(), oracle.normals(out.cpu().numpy(), K))
+    c = torch.full((33, 70), 1.25, device=DEV)
+    out, _ = pm.adf_filter(c, K, 0.25, 0.03, 30)
+    assert torch.equal(out, c)
+
+
+def test_adf_bitwise_invariance_to_blocking_and_batch(pm):
+    # identical arithmetic per sweep -> bitwise independent of
+    # the iterations fused per pass and of batching
+    fr = scenegen.make_config("C2", W=320, H=240)
+    d = fr["depth"].to(DEV)
+    ref, nref = pm.adf_filter(d, fr["K"], fr["lam"], fr["kappa"], 17, iters_per_pass=1)
+    for T in (2, 3, 4, 5, 8, 16):
+        out, nrm = pm.adf_filter(d, fr["K"], fr["lam"], fr["kappa"], 17, iters_per_pass=T)
+        assert torch.equal(out, ref), T
+        assert torch.equal(nrm, nref), T
+    batch = torch.stack([d, d.flip(0), d])
+    out, nrm = pm.adf_filter(batch.contiguous(), fr["K"], fr["lam"], fr["kappa"], 17)
+    assert torch.equal(out[0], ref) and torch.equal(out[2], ref) and torch.equal(nrm[2], nref)
+    o1, _ = pm.adf_filter(d.flip(0).contiguous(), fr["K"], fr["lam"], fr["kappa"], 17)
+    assert torch.equal(out[1], o1)
+
+
+def _ransac_compare(pm, depth_np, labels_np, K, R, H, tau, seed, frame_id=0, sampler=0, select=0):
+    planes, counts, errq = pm.ransac_planes(torch.from_numpy(depth_np).to(DEV), K,
+                                            torch.from_numpy(labels_np).to(DEV), R, H, tau, seed,
+                                            first_frame_id=frame_id, sampler=sampler, select=select, debug=True)
+    torch.cuda.synchronize()
+    ref = oracle.ransac(depth_np, labels_np, K, R, H, tau, seed, frame_id=frame_id, sampler=sampler,
+                        select=select, debug=True)
+    cg = counts.cpu().numpy()
+    assert np.array_equal(cg, ref["counts"]), "per-hypothesis inlier counts must be bit-exact"
+    assert np.array_equal(errq.cpu().numpy().view(np.uint64), ref["errq_all"]), "fixed-point error sums"
+    assert np.array_equal(planes.n_points.cpu().numpy(), ref["n_points"])
+    assert np.array_equal(planes.best_hyp.cpu().numpy(), ref["best_hyp"])
+    assert np.array_equal(planes.status.cpu().numpy(), ref["status"])
+    assert np.array_equal(planes.inliers.cpu().numpy(), ref["inliers"])
+    ok = ref["status"] <= 1
+    if ok.any():
+        assert np.abs(planes.n.cpu().numpy()[ok] - ref["n"][ok]).max() <= REFIT_TOL
+        assert np.abs(planes.d.cpu().numpy()[ok] - ref["d"][ok]).max() <= REFIT_TOL
+        assert np.abs(planes.centroid.cpu().numpy()[ok] - ref["centroid"][ok]).max() <= REFIT_TOL
+        sd = planes.sum_dist.cpu().numpy()[ok].astype(np.float64)
+        want = ref["errq"][ok].astype(np.float64) / 2**24
+        assert np.allclose(sd, want, rtol=1e-6, atol=1e-6)
+    return ref
+
+
+@pytest.mark.parametrize("name,kw,filtered", [
+    ("C1", {}, False), ("C1n", {}, True), ("C1n", {"holes": 0.02}, True), ("C2", {}, False),
+    ("C2", {}, True), ("C2", {"holes": 0.01}, True), ("C2", {"W": 333, "H": 251}, True)])
+def test_ransac_bit_exact(pm, name, kw, filtered):
+    fr = scenegen.make_config(name, **kw)
+    d = fr["depth"]
+    if filtered:                                  # the GPU-filtered frame, shared by both sides
+        d, _ = pm.adf_filter(d.to(DEV), fr["K"], fr["lam"], fr["kappa"], fr["iters"], normals=False)
+        d = d.cpu()
+    _ransac_compare(pm, d.numpy(), fr["labels"].numpy(), fr["K"], fr["n_regions"], fr["n_hyp"], fr["tau"],
+                    fr["seed"])
+
+
+def test_ransac_noise_free_plane(pm):
+    fr = scenegen.make_config("RAMP")
+    lab = np.where(fr["depth"].numpy() > 0, 0, -1).astype(np.int32)
+    ref = _ransac_compare(pm, fr["depth"].numpy(), lab, fr["K"], 1, 64, fr["tau"], fr["seed"])
+    assert ref["status"][0] == 0 and ref["inliers"][0] == ref["n_points"][0]
+
+
+def test_ransac_enumerate_and_select_error(pm):
+    fr = scenegen.make_config("C1n", holes=0.3)
+    d = fr["depth"].numpy()
+    lab = fr["labels"].numpy().copy()
+    # shrink regions to tiny point sets so that ENUMERATE covers all triples
+    keep = np.zeros_like(lab, bool)
+    keep[::7, ::5] = True
+    lab[~keep] = -1
+    ref = oracle.ransac(d, lab, fr["K"], 4, 1, fr["tau"], 1)
+    nmax = int(ref["n_points"].max())
+    _ransac_compare(pm, d, lab, fr["K"], 4, math.comb(nmax, 3), fr["tau"], 1, sampler=1)
+    _ransac_compare(pm, d, fr["labels"].numpy(), fr["K"], 4, 64, fr["tau"], 9, select=1)
+
+
+def test_ransac_frame_ids_and_batch_invariance(pm):
+    d, lab, K = scenegen.stair_stream(10, 3, W=160, H=120, n_regions=16)
+    planes = pm.ransac_planes(d.to(DEV), K, lab.to(DEV), 16, 32, 0.01, 77, first_frame_id=10)
+    torch.cuda.synchronize()
+    for i in range(3):
+        ref = oracle.ransac(d[i].numpy(), lab[i].numpy(), K, 16, 32, 0.01, 77, frame_id=10 + i)
+        assert np.array_equal(planes.best_hyp[i].cpu().numpy(), ref["best_hyp"])
+        assert np.array_equal(planes.inliers[i].cpu().numpy(), ref["inliers"])
+        single = pm.ransac_planes(d[i].contiguous().to(DEV), K, lab[i].contiguous().to(DEV), 16, 32, 0.01, 77,
+                                  first_frame_id=10 + i)
+        assert torch.equal(single.raw, planes.raw[i])
+
+
+def test_ransac_degenerate_cases(pm):
+    K = scenegen.intrinsics_for(64, 48)
+    depth = np.full((48, 64), 1.5, np.float32)
+    lab = np.full((48, 64), -1, np.int32)
+    lab[3, 4] = lab[7, 9] = 0                  # 2 points -> TOO_FEW
+    lab[10, 5:20] = 1                          # collinear -> DEGENERATE
+    lab[20:30, 20:30] = 3                      # plane -> OK
+    lab[40, 40] = 99                           # out-of-range label: ignored
+    ref = _ransac_compare(pm, depth, lab, K, 5, 16, 0.01, 1)
+    assert list(ref["status"]) == [2, 3, 2, 0, 2]
+
+
+def test_pipeline_end_to_end(pm):
+    fr = scenegen.make_config("C2")
+    dev = torch.device(DEV)
+    d_out, nrm, planes = pm.process_frames(fr["depth"].to(dev), fr["labels"].to(dev), fr["K"], fr["lam"],
+                                           fr["kappa"], fr["iters"], fr["n_regions"], fr["n_hyp"], fr["tau"],
+                                           fr["seed"])
+    torch.cuda.synchronize()
+    d_gpu = d_out.cpu().numpy()
+    ref = oracle.ransac(d_gpu, fr["labels"].numpy(), fr["K"], fr["n_regions"], fr["n_hyp"], fr["tau"], fr["seed"])
+    assert np.array_equal(planes.best_hyp.cpu().numpy(), ref["best_hyp"])
+    assert np.array_equal(planes.status.cpu().numpy(), ref["status"])
+    assert (ref["status"] == 0).mean() > 0.9
