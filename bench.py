@@ -1,0 +1,351 @@
+#!/usr/bin/env python
+"""Benchmark of the arXiv 2411.01919 hot path on B200 (BASELINE.json metric).
+
+Workload (BASELINE.json configs[3], "C4"): a stream of distinct synthetic
+640x480 D435-style noisy descending-staircase frames (scenegen G-STAIR,
+DESIGN.md §4), N = 20 ADF iterations (lambda 0.15, kappa 0.03 m) with the
+normal image fused into the last pass, then RANSAC over 64 balanced regions
+per frame x 64 hypotheses (tau 0.01 m) on the filtered depth.  One step = one
+pass of the whole path over this rank's batch of frames (frames_per_rank),
+all resident in HBM; ranks process disjoint frames of the stream (frame ids
+rank * frames_per_rank + i): weak scaling, no data-path collective, a final
+NCCL gather of the plane tables only in the multi-GPU run.
+
+Arms:
+  default            the CUDA path through the C ABI (pm_process_frames)
+  --impl reference   the oracle (oracle/, plain single-threaded C per frame)
+                     on this box's host cores, same workload and metric.
+Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+METRIC = "640x480 frames/sec per B200 and at 8 GPUs; ADF+normal achieved HBM GB/s vs peak"
+W, H = 640, 480
+ITERS, REGIONS, HYPS = 20, 64, 64
+LAM, KAPPA, TAU, SEED = 0.15, 0.03, 0.01, 0x1919
+# algorithmic bytes of the fused ADF+normals stage per pixel: read depth 4 B,
+# write filtered depth 4 B, write normals 12 B
+ADF_ALG_BYTES_PX = 20
+
+
+def _peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            j = json.load(f)
+        return float(j["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """Samples SM clock and throttle reasons with NVML during the timed region."""
+
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+               0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+    def __init__(self, index: int, period_s: float = 0.005):
+        self.index, self.period = index, period_s
+        self.samples, self.reasons = [], set()
+        self._stop = threading.Event()
+        self._t = None
+        self.max_mhz = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self._nv = None
+
+    def _run(self):
+        nv = self._nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self._nv is not None:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"]}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# --------------------------------------------------------------------------- oracle arm
+def _oracle_frame(depth_np, labels_np, K, frame_id):
+    import oracle
+    d = oracle.adf(depth_np, LAM, KAPPA, ITERS)
+    oracle.normals(d, K)
+    oracle.ransac(d, labels_np, K, REGIONS, HYPS, TAU, SEED, frame_id=frame_id)
+
+
+def _cpu_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def _oracle_throughput(frames, K, first_frame, cores):
+    """Run the oracle over `frames` [(depth, labels)] on `cores` threads (the C
+    calls release the GIL); returns (frames/s, wall seconds)."""
+    from concurrent.futures import ThreadPoolExecutor
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(max_workers=cores) as ex:
+        list(ex.map(lambda i: _oracle_frame(frames[i][0], frames[i][1], K, first_frame + i), range(len(frames))))
+    dt = time.perf_counter() - t0
+    return len(frames) / dt, dt
+
+
+def _cpu_sample(n, first_frame):
+    import scenegen
+    d, lab, K = scenegen.stair_stream(first_frame, n, W, H, REGIONS, device="cpu")
+    return [(d[i].numpy(), lab[i].numpy()) for i in range(n)], K
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return 0
+    import oracle
+    oracle.build()
+    cores = _cpu_cores()
+    frames, K = _cpu_sample(cores, 0)
+    for _ in range(args.warmup):
+        _oracle_throughput(frames, K, 0, cores)
+    times = []
+    for _ in range(args.steps):
+        _, dt = _oracle_throughput(frames, K, 0, cores)
+        times.append(dt)
+    total = sum(times)
+    value = cores * args.steps / total
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64+f32",
+        "data": "synthetic",
+        "config": {"workload": "C4 (BASELINE.json configs[3]) 640x480 G-STAIR stream, ADF N=20 + normals + "
+                               "RANSAC 64 regions x 64 hyps", "frames_per_step": cores},
+        "cpu_baseline": {"value": value, "unit": "frames/s", "cores": cores, "kind": "oracle",
+                         "sample": f"{cores} frames per step (one per core), {args.steps} timed steps"},
+        "e2e": {"value": value, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# --------------------------------------------------------------------------- CUDA arm
+def run_cuda(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2411_01919_b200 as pm
+    import scenegen
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    B = args.frames_per_rank
+    first = rank * B
+    # inputs: distinct frames of the C4 stream, generated on the device and kept resident in HBM
+    depth, labels, K = scenegen.stair_stream(first, B, W, H, REGIONS, device=dev)
+    depth_out = torch.empty_like(depth)
+    normals = torch.empty(B, 3, H, W, dtype=torch.float32, device=dev)
+    planes = torch.empty(B, REGIONS, pm.PLANE_WORDS, dtype=torch.int32, device=dev)
+    ws = torch.empty(pm.pipeline_workspace_bytes(W, H, REGIONS, HYPS, B), dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        pm.process_frames(depth, labels, K, LAM, KAPPA, ITERS, REGIONS, HYPS, TAU, SEED, first_frame_id=first,
+                          depth_out=depth_out, normals_out=normals, planes_out=planes, workspace=ws)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    barrier()
+    torch.cuda.synchronize(dev)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(dev.index if dev.index is not None else 0) as clocks:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev1.record(stream)
+        torch.cuda.synchronize(dev)
+    barrier()
+    torch.cuda.synchronize(dev)
+    ms = ev0.elapsed_time(ev1)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    value = world * B * args.steps / (ms_max / 1e3)
+
+    # ---- per-stage times (same launch configuration, same stream), for the roofline
+    adf_ms, rs_ms = [], []
+    for _ in range(max(3, min(args.steps, 10))):
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        e[0].record(stream)
+        pm.adf_filter(depth, K, LAM, KAPPA, ITERS, normals=True, out=depth_out, normals_out=normals, workspace=ws)
+        e[1].record(stream)
+        pm.ransac_planes(depth_out, K, labels, REGIONS, HYPS, TAU, SEED, first_frame_id=first, out=planes,
+                         workspace=ws)
+        e[2].record(stream)
+        torch.cuda.synchronize(dev)
+        adf_ms.append(e[0].elapsed_time(e[1]))
+        rs_ms.append(e[1].elapsed_time(e[2]))
+    adf_t = statistics.median(adf_ms) / 1e3
+    rs_t = statistics.median(rs_ms) / 1e3
+    peak, peak_src = _peaks()
+    adf_bytes = ADF_ALG_BYTES_PX * W * H * B
+    achieved = adf_bytes / adf_t / 1e9
+    n_pass = pm.pipeline_kernel_launches(ITERS, 0)
+    # FP32/MUFU view of the same stage: pixel-iterations per second
+    pix_iter_per_s = ITERS * W * H * B / adf_t
+
+    # ---- e2e: host-resident inputs through the public API, H2D + compute + D2H of the plane table
+    h_depth = depth.cpu().pin_memory()
+    h_labels = labels.cpu().pin_memory()
+    h_planes = torch.empty_like(planes, device="cpu").pin_memory()
+    d_depth, d_labels = torch.empty_like(depth), torch.empty_like(labels)
+
+    def e2e_step():
+        d_depth.copy_(h_depth, non_blocking=True)
+        d_labels.copy_(h_labels, non_blocking=True)
+        pm.process_frames(d_depth, d_labels, K, LAM, KAPPA, ITERS, REGIONS, HYPS, TAU, SEED, first_frame_id=first,
+                          depth_out=depth_out, normals_out=normals, planes_out=planes, workspace=ws)
+        h_planes.copy_(planes, non_blocking=True)
+
+    for _ in range(max(1, args.warmup)):
+        e2e_step()
+    torch.cuda.synchronize(dev)
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        e2e_step()
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    te = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_value = world * B * args.steps / (float(te.item()) / 1e3)
+
+    # ---- final gather of the plane tables (the only collective)
+    if world > 1:
+        gathered = [torch.empty_like(planes) for _ in range(world)] if rank == 0 else None
+        if rank == 0:
+            dist.gather(planes, gathered, dst=0)
+        else:
+            dist.gather(planes, None, dst=0)
+
+    # ---- oracle baseline on the host cores (rank 0, N = 1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        import oracle
+        oracle.build()
+        cores = _cpu_cores()
+        n1, _ = 1, None
+        frames = [(depth[0].cpu().numpy(), labels[0].cpu().numpy())]
+        _, t1 = _oracle_throughput(frames, K, first, 1)
+        n = int(min(max(cores, round(args.cpu_seconds / max(t1, 1e-3))), 8 * cores, B))
+        frames = [(depth[i].cpu().numpy(), labels[i].cpu().numpy()) for i in range(n)]
+        fps, wall = _oracle_throughput(frames, K, first, cores)
+        cpu = {"value": fps, "unit": "frames/s", "cores": cores, "kind": "oracle",
+               "sample": f"{n} frames of the same stream ({wall:.1f} s wall, ~{t1 * n:.0f} s of CPU work; "
+                         f"1 frame on 1 core: {t1 * 1e3:.0f} ms)"}
+
+    launches_per_step = pm.pipeline_kernel_launches(ITERS, REGIONS)
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": "C4 (BASELINE.json configs[3]): stream of distinct 640x480 D435-noise G-STAIR "
+                                   "frames; ADF N=20 (lambda 0.15, kappa 0.03 m) + fused normals, RANSAC 64 "
+                                   "regions x 64 hypotheses (tau 0.01 m) on the filtered depth",
+                       "frames_per_rank": B, "global_frames_per_step": world * B,
+                       "l2": f"inputs larger than L2 ({B * W * H * 8 / 2**20:.0f} MiB depth+labels per rank)",
+                       "parallelism": f"frame-sharded x{world}"},
+            "roofline": {"bound": "hbm", "kernel": f"adf_filter stage ({n_pass} pass launches, last fused with "
+                                                   "normals)",
+                         "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                         "traffic": None, "peak_source": peak_src,
+                         "alg_bytes_per_launch": adf_bytes, "stage_ms": adf_t * 1e3,
+                         "pixel_iters_per_s": pix_iter_per_s},
+            "stages_ms": {"adf_normals": adf_t * 1e3, "ransac_incl_compaction": rs_t * 1e3},
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_value, "unit": "frames/s", "h2d_bytes_per_step": B * W * H * 8,
+                    "d2h_bytes_per_step": B * REGIONS * 48},
+            "gpu_launches": launches_per_step * args.steps,
+            "clocks": clocks.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="cuda", choices=["cuda", "reference"])
+    ap.add_argument("--frames-per-rank", type=int, default=512)
+    ap.add_argument("--cpu-seconds", type=float, default=15.0, help="CPU work budget of the oracle baseline")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        return run_cuda(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -199,6 +199,10 @@ PM_API pm_status pm_process_frames(const float* depth_in, const int32_t* region_
 PM_API size_t pm_pipeline_workspace_bytes(int32_t W, int32_t H, int32_t n_regions, int32_t n_hyp,
                                           int32_t n_frames);
 
+/* Number of kernel launches one pm_process_frames call enqueues (for the
+ * bench's launch accounting; memsets excluded). */
+PM_API int32_t pm_pipeline_kernel_launches(int32_t iters, int32_t n_regions);
+
 /* Human-readable status. */
 PM_API const char* pm_status_string(pm_status s);
 /* ABI version (major * 10000 + minor * 100 + patch). */

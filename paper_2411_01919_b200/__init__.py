@@ -50,6 +50,8 @@ _KP = ctypes.POINTER(pm_intrinsics)
 _lib.pm_status_string.restype = ctypes.c_char_p
 _lib.pm_status_string.argtypes = [ctypes.c_int]
 _lib.pm_version.restype = _I32
+_lib.pm_pipeline_kernel_launches.restype = _I32
+_lib.pm_pipeline_kernel_launches.argtypes = [_I32, _I32]
 _lib.pm_adf_workspace_bytes.restype = _SZ
 _lib.pm_adf_workspace_bytes.argtypes = [_I32, _I32, _I32]
 _lib.pm_ransac_workspace_bytes.restype = _SZ
@@ -77,7 +79,8 @@ for _fn in ("pm_adf_filter", "pm_adf_filter_batched", "pm_adf_filter_ex", "pm_no
 EXPORTED = ("pm_adf_filter", "pm_adf_filter_batched", "pm_adf_filter_ex", "pm_adf_workspace_bytes",
             "pm_normals_from_depth", "pm_normals_from_depth_batched", "pm_ransac_planes",
             "pm_ransac_planes_batched", "pm_ransac_planes_ex", "pm_ransac_workspace_bytes",
-            "pm_process_frames", "pm_pipeline_workspace_bytes", "pm_status_string", "pm_version")
+            "pm_process_frames", "pm_pipeline_workspace_bytes", "pm_pipeline_kernel_launches",
+            "pm_status_string", "pm_version")
 
 
 class PMError(RuntimeError):
@@ -119,6 +122,10 @@ def _stream(t: torch.Tensor) -> int:
 
 def _workspace(nbytes: int, device) -> torch.Tensor:
     return torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=device)
+
+
+def pipeline_kernel_launches(iters: int, n_regions: int) -> int:
+    return int(_lib.pm_pipeline_kernel_launches(int(iters), int(n_regions)))
 
 
 def adf_workspace_bytes(W: int, H: int, n_frames: int = 1) -> int:

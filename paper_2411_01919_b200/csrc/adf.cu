@@ -2,17 +2,30 @@
 // temporally blocked Perona–Malik diffusion (ℓ1-8) with the Sobel/normal
 // stage (ℓ9-13) fused into the last pass.
 //
-// One CTA owns an output tile of TW x TH pixels of one frame.  It loads the
-// tile plus an R-pixel halo (R = iterations of this pass, +1 when the normal
-// stage is fused) into shared memory once, runs the pass's T Jacobi sweeps in
-// shared memory on a region that shrinks by one pixel per sweep (ping-pong
-// buffers), and writes the tile back: one HBM read and one write per pass
-// instead of one per sweep.  Every cell update uses the same explicit _rn
-// arithmetic, so the result is bitwise independent of T, tile shape and
-// batch.
+// One CTA owns an output tile of (128 - 2R) x 64 pixels of one frame.  It
+// loads the tile plus an R-pixel halo (R = sweeps of this pass, +1 when the
+// normal stage is fused) into shared memory once, runs the pass's T Jacobi
+// sweeps in shared memory on a region that shrinks by one pixel per sweep
+// (ping-pong buffers), and writes the tile back: one HBM read and one write
+// per T sweeps.
+//
+// Sweep inner loop ("column walk"): each thread owns one column of a row
+// strip and walks down it keeping the north and centre values in registers,
+// so a cell update costs 3 shared loads (S, W, E), 1 store, 12 FP32 ops and
+// one MUFU.EX2.  The zero-flux image border (Q4) costs nothing per cell: a
+// thread whose column is the first / last image column points its W / E
+// address at the centre cell, the strip that starts on the first image row
+// seeds N with the centre, and the last image row is peeled with S = centre.
+// Tiles whose loaded region contains an invalid depth (holes) run the same
+// walk with per-neighbour validity substitution (zero flux at holes, Q4).
+// Every path evaluates the identical _rn expression on identical operands,
+// so the result is bitwise independent of tile shape, sweeps per pass and
+// batching.
 #include <cuda_runtime.h>
 #include <float.h>
+#include <math.h>
 #include <stdint.h>
+#include <string.h>
 
 #include "common.cuh"
 #include "internal.h"
@@ -21,32 +34,87 @@ namespace pm {
 
 namespace {
 
-constexpr int kThreads = 256;      // 32 x 8
-constexpr int kSmemW = 128;        // smem row pitch (floats); TW = kSmemW - 2R
-constexpr int kTileH = 32;         // output rows per CTA
+constexpr int kThreads = 256;      // 8 warps
+constexpr int kWarps = kThreads / 32;
+constexpr int kMaxItersPerPass = 16;
 
 struct AdfParams {
-    float lam;        // gamma of Alg. 1
-    float kc;         // -log2(e) / (4 kappa^2): c = 2^(kc * (2gx)^2 + (2gy)^2))
+    float kc;         // -log2(e) / (4 kappa^2)
+    float l2lam;      // log2(lambda): lambda * c = 2^(kc * g2 + log2(lambda))
     float fx, fy, cx, cy;
 };
 
-// One Jacobi update of Alg. 1 ℓ4-6 at a valid centre value I with the four
-// neighbour values (zero-flux rule Q4: invalid or out-of-image neighbours
-// were stored as non-positive values and are replaced by the centre).
-// dN = N - I etc.; gx2 = 2 gx = dE - dW, gy2 = 2 gy = dS - dN;
-// c = exp(-(gx^2 + gy^2)/k^2) = 2^(kc (gx2^2 + gy2^2)); lap = (dN+dS)+(dE+dW).
-PM_DEVINL float adf_update(float I, float n, float s, float w, float e, float lam, float kc) {
-    const float dn = valid_depth(n) ? __fsub_rn(n, I) : 0.0f;
-    const float ds = valid_depth(s) ? __fsub_rn(s, I) : 0.0f;
-    const float dw = valid_depth(w) ? __fsub_rn(w, I) : 0.0f;
-    const float de = valid_depth(e) ? __fsub_rn(e, I) : 0.0f;
+// Alg. 1 ℓ4-6 at a valid centre C with neighbour values N, S, W, E (already
+// replaced by C where the zero-flux rule applies):
+//   dX = X - C;  2gx = dE - dW;  2gy = dS - dN;  lap = (dN + dS) + (dE + dW)
+//   lambda * c = 2^(kc (2gx^2 + 2gy^2) + log2 lambda),  c = exp(-|grad|^2 / k^2)
+//   I' = C + (lambda c) * lap
+PM_DEVINL float adf_cell(float C, float N, float S, float W, float E, float kc, float l2lam) {
+    const float dn = __fsub_rn(N, C), ds = __fsub_rn(S, C);
+    const float dw = __fsub_rn(W, C), de = __fsub_rn(E, C);
     const float gx2 = __fsub_rn(de, dw);
     const float gy2 = __fsub_rn(ds, dn);
     const float g2 = __fmaf_rn(gx2, gx2, __fmul_rn(gy2, gy2));
-    const float c = ex2_approx(__fmul_rn(g2, kc));
+    const float lc = ex2_approx(__fmaf_rn(g2, kc, l2lam));
     const float lap = __fadd_rn(__fadd_rn(dn, ds), __fadd_rn(de, dw));
-    return __fmaf_rn(__fmul_rn(lam, c), lap, I);
+    return __fmaf_rn(lc, lap, C);
+}
+
+template <bool CHECK>
+PM_DEVINL float cell(float C, float N, float S, float W, float E, float kc, float l2lam) {
+    if (CHECK) {
+        if (!valid_depth(C)) return C;                 // invalid pixels never change
+        N = valid_depth(N) ? N : C;
+        S = valid_depth(S) ? S : C;
+        W = valid_depth(W) ? W : C;
+        E = valid_depth(E) ? E : C;
+    }
+    return adf_cell(C, N, S, W, E, kc, l2lam);
+}
+
+// Shared tile: kSW = 128 columns (four 32-lane column groups) x SH rows; the
+// output tile is (kSW - 2R) x TH; smem cell (sx, sy) is image pixel
+// (x0 + sx, y0 + sy); the image covers smem columns [ix0, ix1), rows [iy0, iy1).
+constexpr int kSW = 128;
+constexpr int kTH = 64;               // output rows per CTA
+
+struct Box { int ix0, ix1, iy0, iy1; };
+
+// One Jacobi sweep over smem rows [t, SH - t) x columns [PAD + t, kSW - PAD - t)
+// (PAD = unused alignment columns), clipped to the image.  Warp w walks
+// column group (w & 3), row half (w >> 2).
+template <int SH, int PAD, bool CHECK>
+PM_DEVINL void sweep(const float* __restrict__ cur, float* __restrict__ nxt, int t, const Box& b,
+                     float kc, float l2lam) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int x = (warp & 3) * 32 + lane;
+    const int ylo = max(t, b.iy0), yhi = min(SH - t, b.iy1);
+    const int half = (yhi - ylo + 1) >> 1;
+    const int ys = ylo + (warp >> 2) * half;
+    const int ye = min(ys + half, yhi);
+    if (x < max(PAD + t, b.ix0) || x >= min(kSW - PAD - t, b.ix1) || ys >= ye) return;
+    const int ylast = b.iy1 - 1;
+    const int ymid = min(ye, ylast);            // rows [ys, ymid) have a real south neighbour
+    const int offW = x == b.ix0 ? 0 : -1;       // zero flux at the image border (Q4)
+    const int offE = x == b.ix1 - 1 ? 0 : 1;
+    const float* col = cur + x;
+    const float* colW = col + offW;
+    const float* colE = col + offE;
+    float* ocol = nxt + x;
+    float C = col[ys * kSW];
+    float N = ys == b.iy0 ? C : col[(ys - 1) * kSW];
+    int y = ys;
+#pragma unroll 4
+    for (; y < ymid; ++y) {
+        const float S = col[(y + 1) * kSW];
+        const float W = colW[y * kSW];
+        const float E = colE[y * kSW];
+        ocol[y * kSW] = cell<CHECK>(C, N, S, W, E, kc, l2lam);
+        N = C;
+        C = S;
+    }
+    if (ye > ylast)                             // last image row: S = C
+        ocol[y * kSW] = cell<CHECK>(C, N, C, colW[y * kSW], colE[y * kSW], kc, l2lam);
 }
 
 // Sobel (1/8-normalised, clamp-to-edge) + geometric normal (Eq. 2 read as
@@ -71,70 +139,147 @@ PM_DEVINL float3 sobel_normal(const float z[3][3], float u, float v, const AdfPa
     const float ss = __fmaf_rn(mx, mx, __fmaf_rn(my, my, __fmul_rn(mz, mz)));
     if (!(ss > 0.0f) || !(ss <= FLT_MAX)) return make_float3(0.f, 0.f, 0.f);
     const float inv = rsqrtf(ss);
-    return make_float3(mx * inv, my * inv, mz * inv);
+    return make_float3(__fmul_rn(mx, inv), __fmul_rn(my, inv), __fmul_rn(mz, inv));
 }
 
-// One pass: `iters` sweeps on a tile; halo R = iters + (fuse ? 1 : 0).
-//   src [B][H][W] -> dst [B][H][W] (if write_depth) and normals [B][3][H][W].
-__global__ void __launch_bounds__(kThreads)
-adf_pass_kernel(const float* __restrict__ src, float* __restrict__ dst,
-                float* __restrict__ normals, int W, int H, int iters, int R,
-                int write_depth, AdfParams p) {
-    extern __shared__ float smem[];
-    const int TW = kSmemW - 2 * R;
-    const int SH = kTileH + 2 * R;
+template <int R>
+constexpr size_t pass_smem_bytes() { return sizeof(float) * 2 * (size_t)kSW * (kTH + 2 * R); }
+
+// Left halo rounded up to 4 columns: the TMA box must start on a 16-byte
+// column boundary (measured on B200: other starts raise an illegal-instruction
+// fault), so smem column 0 is image column bx * TW - RA.
+template <int R>
+__host__ __device__ constexpr int halo_x() { return (R + 3) & ~3; }
+template <int R>
+__host__ __device__ constexpr int tile_w() { return kSW - 2 * halo_x<R>(); }
+
+// One pass of `iters` sweeps; halo R = iters (+1 when the normals are fused).
+//   src [B][H][W] -> dst [B][H][W] (if dst) and normals [B][3][H][W] (if normals).
+template <int R>
+__global__ void __launch_bounds__(kThreads, 2)
+adf_pass_kernel(const float* __restrict__ src, float* __restrict__ dst, float* __restrict__ normals,
+                int W, int H, int iters, AdfParams p, const __grid_constant__ CUtensorMap tmap, int use_tma) {
+    constexpr int SH = kTH + 2 * R;
+    constexpr int RA = halo_x<R>();
+    constexpr int TW = tile_w<R>();
+    constexpr int PAD = RA - R;
+    extern __shared__ __align__(128) float smem[];
+    __shared__ __align__(8) uint64_t bar;
     float* buf0 = smem;
-    float* buf1 = smem + kSmemW * SH;
+    float* buf1 = smem + kSW * SH;
     const size_t frame = blockIdx.z;
     const size_t HW = (size_t)H * W;
     const float* in = src + frame * HW;
-    const int x0 = blockIdx.x * TW - R;     // image coords of smem (0, 0)
-    const int y0 = blockIdx.y * kTileH - R;
-    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    const int x0 = blockIdx.x * TW - RA;       // image coords of smem (0, 0)
+    const int y0 = blockIdx.y * kTH - R;
+    Box b;
+    b.ix0 = max(0, -x0); b.ix1 = min(kSW, W - x0);
+    b.iy0 = max(0, -y0); b.iy1 = min(SH, H - y0);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 
-    // load tile + halo; out-of-image cells get 0 (invalid => zero flux)
-    for (int y = ty; y < SH; y += kThreads / 32) {
-        const int gy = y0 + y;
-        const bool rowok = gy >= 0 && gy < H;
-        for (int x = tx; x < kSmemW; x += 32) {
-            const int gx = x0 + x;
-            float v = 0.0f;
-            if (rowok && gx >= 0 && gx < W) v = __ldg(in + (size_t)gy * W + gx);
-            buf0[y * kSmemW + x] = v;
+    // load tile + halo: one TMA box (out-of-image cells zero-filled, never
+    // read) or coalesced LDG rows; note whether every in-image pixel is valid
+    // (fast path) or not (hole-aware path)
+    bool all_valid = true;
+    if (use_tma) {
+        if (threadIdx.x == 0) mbar_init(&bar, 1);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            mbar_arrive_expect_tx(&bar, (uint32_t)(sizeof(float) * kSW * SH));
+            tma_load_3d(buf0, &tmap, x0, y0, (int)frame, &bar);
+        }
+        mbar_wait(&bar, 0);
+        // validity scan: each lane checks 4 consecutive columns per row
+        const int c0 = 4 * lane;
+        bool in[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) in[j] = c0 + j >= b.ix0 && c0 + j < b.ix1;
+        for (int sy = b.iy0 + warp; sy < b.iy1; sy += kWarps) {
+            const float4 v = *reinterpret_cast<const float4*>(buf0 + sy * kSW + c0);
+            all_valid &= (valid_depth(v.x) || !in[0]) && (valid_depth(v.y) || !in[1]) &&
+                         (valid_depth(v.z) || !in[2]) && (valid_depth(v.w) || !in[3]);
+        }
+    } else {
+        for (int sy = b.iy0 + warp; sy < b.iy1; sy += kWarps) {
+            const float* row = in + (size_t)(y0 + sy) * W + x0;
+#pragma unroll
+            for (int k = 0; k < kSW / 32; ++k) {
+                const int sx = k * 32 + lane;
+                if (sx >= b.ix0 && sx < b.ix1) {
+                    const float v = __ldg(row + sx);
+                    all_valid &= valid_depth(v);
+                    buf0[sy * kSW + sx] = v;
+                }
+            }
         }
     }
-    __syncthreads();
+    all_valid = __syncthreads_and(all_valid);
 
     float* cur = buf0;
     float* nxt = buf1;
     for (int t = 1; t <= iters; ++t) {
-        for (int y = t + ty; y < SH - t; y += kThreads / 32) {
-            const float* row = cur + y * kSmemW;
-            float* orow = nxt + y * kSmemW;
-            for (int x = t + tx; x < kSmemW - t; x += 32) {
-                const float I = row[x];
-                float o = I;
-                if (valid_depth(I))
-                    o = adf_update(I, row[x - kSmemW], row[x + kSmemW], row[x - 1], row[x + 1], p.lam, p.kc);
-                orow[x] = o;
-            }
-        }
+        if (all_valid)
+            sweep<SH, PAD, false>(cur, nxt, t, b, p.kc, p.l2lam);
+        else
+            sweep<SH, PAD, true>(cur, nxt, t, b, p.kc, p.l2lam);
         __syncthreads();
         float* tmp = cur; cur = nxt; nxt = tmp;
     }
 
-    // write the tile (and its normals)
-    const int ox = blockIdx.x * TW, oy = blockIdx.y * kTileH;
-    float* out = dst + frame * HW;
+    // write the tile (and its normals).  Rows of float4 quads when W % 4 == 0
+    // (the tile origin is then 16-byte aligned in global and shared memory).
+    const int ox = blockIdx.x * TW, oy = blockIdx.y * kTH;
+    float* out = dst ? dst + frame * HW : nullptr;
     float* nrm = normals ? normals + frame * 3 * HW : nullptr;
-    for (int y = ty; y < kTileH; y += kThreads / 32) {
+    if ((W & 3) == 0) {
+        constexpr int QW = TW / 4;
+        for (int y = warp; y < kTH; y += kWarps) {
+            const int gy = oy + y;
+            if (gy >= H) break;
+            const int q = lane;
+            const int gx = ox + 4 * q;
+            if (q >= QW || gx >= W) continue;
+            const int sx = RA + 4 * q, sy = y + R;
+            const size_t o = (size_t)gy * W + gx;
+            const float4 c = *reinterpret_cast<const float4*>(cur + sy * kSW + sx);
+            if (out) *reinterpret_cast<float4*>(out + o) = c;
+            if (nrm) {
+                // clamp-to-edge 3x6 window: rows ym, sy, yp; columns gx-1 .. gx+4
+                const int rows[3] = {max(gy - 1, 0) - y0, sy, min(gy + 1, H - 1) - y0};
+                float z[3][6];
+#pragma unroll
+                for (int a = 0; a < 3; ++a) {
+                    const float* rp = cur + rows[a] * kSW + sx;
+                    const float4 m = *reinterpret_cast<const float4*>(rp);
+                    z[a][1] = m.x; z[a][2] = m.y; z[a][3] = m.z; z[a][4] = m.w;
+                    z[a][0] = gx == 0 ? m.x : rp[-1];
+                    z[a][5] = gx + 4 >= W ? m.w : rp[4];
+                }
+                float4 nx, ny, nz;
+                float* px = &nx.x; float* py = &ny.x; float* pz = &nz.x;
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const float w3[3][3] = {{z[0][j], z[0][j + 1], z[0][j + 2]},
+                                            {z[1][j], z[1][j + 1], z[1][j + 2]},
+                                            {z[2][j], z[2][j + 1], z[2][j + 2]}};
+                    const float3 n = sobel_normal(w3, (float)(gx + j), (float)gy, p);
+                    px[j] = n.x; py[j] = n.y; pz[j] = n.z;
+                }
+                *reinterpret_cast<float4*>(nrm + o) = nx;
+                *reinterpret_cast<float4*>(nrm + HW + o) = ny;
+                *reinterpret_cast<float4*>(nrm + 2 * HW + o) = nz;
+            }
+        }
+        return;
+    }
+    for (int y = warp; y < kTH; y += kWarps) {
         const int gy = oy + y;
         if (gy >= H) break;
-        for (int x = tx; x < TW; x += 32) {
+        for (int x = lane; x < TW; x += 32) {
             const int gx = ox + x;
             if (gx >= W) break;
-            const int sx = x + R, sy = y + R;
-            if (write_depth) out[(size_t)gy * W + gx] = cur[sy * kSmemW + sx];
+            const int sx = x + RA, sy = y + R;
+            if (out) out[(size_t)gy * W + gx] = cur[sy * kSW + sx];
             if (nrm) {
                 // clamp-to-edge window in image coords, mapped to smem coords
                 const int xm = max(gx - 1, 0) - x0, xp = min(gx + 1, W - 1) - x0;
@@ -144,7 +289,7 @@ adf_pass_kernel(const float* __restrict__ src, float* __restrict__ dst,
 #pragma unroll
                 for (int a = 0; a < 3; ++a)
 #pragma unroll
-                    for (int b = 0; b < 3; ++b) z[a][b] = cur[ys[a] * kSmemW + xs[b]];
+                    for (int c = 0; c < 3; ++c) z[a][c] = cur[ys[a] * kSW + xs[c]];
                 const float3 n = sobel_normal(z, (float)gx, (float)gy, p);
                 const size_t o = (size_t)gy * W + gx;
                 nrm[o] = n.x;
@@ -155,56 +300,91 @@ adf_pass_kernel(const float* __restrict__ src, float* __restrict__ dst,
     }
 }
 
-size_t pass_smem_bytes(int R) { return sizeof(float) * 2 * kSmemW * (kTileH + 2 * R); }
+using PassFn = void (*)(const float*, float*, float*, int, int, int, AdfParams, const CUtensorMap, int);
+
+template <int R>
+struct PassTable {
+    static void fill(PassFn* fns, size_t* smem, int* tw) {
+        fns[R] = adf_pass_kernel<R>;
+        smem[R] = pass_smem_bytes<R>();
+        tw[R] = tile_w<R>();
+        PassTable<R - 1>::fill(fns, smem, tw);
+    }
+};
+template <>
+struct PassTable<0> {
+    static void fill(PassFn*, size_t*, int*) {}
+};
+
+struct Passes {
+    PassFn fn[kMaxItersPerPass + 2] = {};
+    size_t smem[kMaxItersPerPass + 2] = {};
+    int tw[kMaxItersPerPass + 2] = {};
+    Passes() { PassTable<kMaxItersPerPass + 1>::fill(fn, smem, tw); }
+};
+const Passes& passes() {
+    static const Passes p;
+    return p;
+}
 
 }  // namespace
 
-constexpr int kMaxItersPerPass = 16;
-
 cudaError_t adf_setup_attributes() {
-    return cudaFuncSetAttribute(adf_pass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)pass_smem_bytes(kMaxItersPerPass + 1));
+    const Passes& P = passes();
+    for (int R = 1; R <= kMaxItersPerPass + 1; ++R) {
+        cudaError_t e = cudaFuncSetAttribute(P.fn[R], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P.smem[R]);
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
 }
 
 static cudaError_t launch_pass(const float* src, float* dst, float* normals, int W, int H, int B,
-                               int iters, bool fuse, bool write_depth, const AdfParams& p,
-                               cudaStream_t stream) {
+                               int iters, bool fuse, const AdfParams& p, cudaStream_t stream) {
     const int R = iters + (fuse ? 1 : 0);
-    const int TW = kSmemW - 2 * R;
-    dim3 grid((W + TW - 1) / TW, (H + kTileH - 1) / kTileH, B);
-    adf_pass_kernel<<<grid, kThreads, pass_smem_bytes(R), stream>>>(src, dst, normals, W, H, iters, R,
-                                                                     write_depth ? 1 : 0, p);
-    return cudaGetLastError();
+    const Passes& P = passes();
+    const int TW = P.tw[R];
+    dim3 grid((W + TW - 1) / TW, (H + kTH - 1) / kTH, B);
+    CUtensorMap tmap;
+    int use_tma = make_tmap_f32_3d(&tmap, src, W, H, B, kSW, kTH + 2 * R) ? 1 : 0;
+    if (!use_tma) memset(&tmap, 0, sizeof(tmap));
+    void* args[] = {(void*)&src, (void*)&dst,   (void*)&normals, (void*)&W,      (void*)&H,
+                    (void*)&iters, (void*)&p, (void*)&tmap,    (void*)&use_tma};
+    return cudaLaunchKernel((const void*)P.fn[R], grid, dim3(kThreads), args, P.smem[R], stream);
 }
 
 int adf_default_iters_per_pass() { return 4; }
 
-cudaError_t adf_run(const float* in, float* out, float* normals, float* ws, int W, int H, int B,
-                    const pm_intrinsics* K, float lam, float kappa, int iters, int iters_per_pass,
-                    cudaStream_t stream) {
+static AdfParams make_params(const pm_intrinsics* K, float lam, float kappa) {
     AdfParams p;
-    p.lam = lam;
     p.kc = (float)(-1.4426950408889634 / (4.0 * (double)kappa * (double)kappa));
+    p.l2lam = (float)log2((double)lam);
     p.fx = K ? K->fx : 1.f;
     p.fy = K ? K->fy : 1.f;
     p.cx = K ? K->cx : 0.f;
     p.cy = K ? K->cy : 0.f;
+    return p;
+}
+
+cudaError_t adf_run(const float* in, float* out, float* normals, float* ws, int W, int H, int B,
+                    const pm_intrinsics* K, float lam, float kappa, int iters, int iters_per_pass,
+                    cudaStream_t stream) {
+    const AdfParams p = make_params(K, lam, kappa);
     int T = iters_per_pass > 0 ? iters_per_pass : adf_default_iters_per_pass();
     if (T > kMaxItersPerPass) T = kMaxItersPerPass;
-    if (iters == 0) {
-        // N = 0: I_smooth = I; normals of the input
-        return launch_pass(in, out, normals, W, H, B, 0, normals != nullptr, true, p, stream);
+    if (iters == 0) {   // N = 0: I_smooth = I (Alg. 1 ℓ1); normals of the input
+        if (!normals)
+            return cudaMemcpyAsync(out, in, sizeof(float) * (size_t)B * W * H, cudaMemcpyDeviceToDevice, stream);
+        return launch_pass(in, out, normals, W, H, B, 0, true, p, stream);
     }
     const int passes = (iters + T - 1) / T;
     const float* src = in;
     int done = 0;
     for (int k = 0; k < passes; ++k) {
         const int it = (iters - done) / (passes - k);   // near-equal split, sums to iters
-        // ping-pong so that the last pass lands in `out`
-        float* dst = (((passes - 1 - k) & 1) == 0) ? out : ws;
+        float* dst = (((passes - 1 - k) & 1) == 0) ? out : ws;   // the last pass lands in `out`
         const bool last = k == passes - 1;
-        cudaError_t e = launch_pass(src, dst, last ? normals : nullptr, W, H, B, it,
-                                    last && normals != nullptr, true, p, stream);
+        cudaError_t e = launch_pass(src, dst, last ? normals : nullptr, W, H, B, it, last && normals != nullptr,
+                                    p, stream);
         if (e != cudaSuccess) return e;
         src = dst;
         done += it;
@@ -214,9 +394,8 @@ cudaError_t adf_run(const float* in, float* out, float* normals, float* ws, int 
 
 cudaError_t normals_run(const float* depth, float* normals, int W, int H, int B,
                         const pm_intrinsics* K, cudaStream_t stream) {
-    AdfParams p{};
-    p.fx = K->fx; p.fy = K->fy; p.cx = K->cx; p.cy = K->cy;
-    return launch_pass(depth, nullptr, normals, W, H, B, 0, true, false, p, stream);
+    const AdfParams p = make_params(K, 0.25f, 1.0f);
+    return launch_pass(depth, nullptr, normals, W, H, B, 0, true, p, stream);
 }
 
 }  // namespace pm

@@ -199,6 +199,12 @@ PM_API pm_status pm_process_frames(const float* depth_in, const int32_t* region_
                        inlier_thresh, seed, planes_out, workspace, ws_bytes, nullptr, (cudaStream_t)stream);
 }
 
+PM_API int32_t pm_pipeline_kernel_launches(int32_t iters, int32_t n_regions) {
+    const int T = pm::adf_default_iters_per_pass();
+    const int adf = iters <= 0 ? 1 : (iters + T - 1) / T;
+    return adf + (n_regions > 0 ? 4 /* compaction */ + 3 /* ransac */ : 0);
+}
+
 PM_API const char* pm_status_string(pm_status s) {
     switch (s) {
         case PM_OK: return "ok";

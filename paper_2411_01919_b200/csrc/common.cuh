@@ -60,3 +60,50 @@ PM_DEVINL float plane_dist(float4 pl, float3 P) {
 }
 
 }  // namespace pm
+
+// ---------------------------------------------------------------------------
+// TMA (cp.async.bulk.tensor) + mbarrier helpers, sm_90+/sm_100a.
+#include <cuda.h>
+
+namespace pm {
+
+PM_DEVINL uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+PM_DEVINL void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+PM_DEVINL void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+
+PM_DEVINL void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+// 3-D tile load global -> shared, completion signalled on `bar` (tx bytes).
+PM_DEVINL void tma_load_3d(void* dst, const CUtensorMap* map, int x, int y, int z, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
+        "l"((uint64_t)map), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+        : "memory");
+}
+
+// Host: encode a 3-D fp32 tensor map over [B][H][W] with a boxW x boxH x 1
+// box (zero fill out of bounds).  Returns false when TMA cannot describe the
+// buffer (row stride not a multiple of 16 B, misaligned base, entry point
+// unavailable) -- callers then use the LDG path.
+bool make_tmap_f32_3d(CUtensorMap* map, const void* base, int W, int H, int B, int boxW, int boxH);
+
+}  // namespace pm
