@@ -19,9 +19,10 @@ cudaError_t normals_run(const float* depth, float* normals, int W, int H, int B,
                         const pm_intrinsics* K, cudaStream_t stream);
 
 // ---- compact.cu / ransac.cu
+struct Sums;
 struct RansacWorkspace {
     // sizes
-    int W, H, B, R, n_hyp, n_hyp_pad, sub_tile, n_sub;
+    int W, H, B, R, n_hyp, n_hyp_pad, sub_tile, n_sub, n_slots;
     // buffers (device)
     uint2* points;        // [B][W*H] packed (u | v<<16, z bits), region-major, raster order
     int32_t* hist;        // [B][R][n_sub] count -> exclusive prefix per region
@@ -30,6 +31,7 @@ struct RansacWorkspace {
     float4* planes;       // [B][R][n_hyp_pad] hypothesis planes (NaN = invalid)
     int32_t* counts;      // [B][R][n_hyp_pad] inlier counts (-1 = invalid)
     uint64_t* errq;       // [B][R][n_hyp_pad] fixed-point error sums (select=ERROR / debug)
+    Sums* slots;          // [B][n_slots] refit moments per (region, chunk): slot chunk + region
     size_t total_bytes;
 };
 // Carve `base` (nullable: sizing only) into the ransac workspace.

@@ -23,13 +23,21 @@
 
 namespace pm {
 
+// fp64 refit moments of one (region, chunk) slot (declared in internal.h)
+struct __align__(16) Sums {
+    double s[3];     // sum of q = p - o over inliers (o = the region's first point)
+    double m[6];     // sum of q q^T (xx, xy, xz, yy, yz, zz)
+    unsigned long long err;   // sum over ALL points of rint(min(d, 64) * 2^24)
+    int n;           // inliers
+    int pad;
+};
+
 namespace {
 
 constexpr unsigned kFull = 0xFFFFFFFFu;
 constexpr int kScoreThreads = 256;
 constexpr int kChunk = 2048;          // points per scoring CTA
 constexpr int kHB = 8;                // hypotheses per register block
-constexpr int kSelectThreads = 256;
 
 struct SampleIdx { uint32_t i0, i1, i2; bool ok; };
 
@@ -114,39 +122,63 @@ ransac_hyp_kernel(RansacWorkspace ws, RansacArgs a, int need_err) {
     if (need_err) ws.errq[slot] = 0ull;
 }
 
-// The hot loop.  grid = (ceil(W*H / kChunk), B).
+// ---- chunk staging shared by the score and refit kernels: the compacted
+// points [s, e) of frame f, deprojected once into shared memory, and the
+// first region overlapping the chunk.
+struct Chunk {
+    int s, e, r0;
+};
+
+PM_DEVINL bool stage_chunk(const RansacWorkspace& ws, const RansacArgs& a, size_t f, float4* sp, int* s_r0,
+                           Chunk& ck) {
+    const int R = ws.R;
+    const int32_t* off = ws.region_off + f * (size_t)(R + 1);
+    const int total = off[R];
+    ck.s = blockIdx.x * kChunk;
+    if (ck.s >= total) return false;
+    ck.e = min(ck.s + kChunk, total);
+    const uint2* pts = ws.points + f * (size_t)ws.W * ws.H;
+    const float ifx = 1.0f / a.K.fx, ify = 1.0f / a.K.fy;   // IEEE division, as on the host
+    for (int i = threadIdx.x; i < ck.e - ck.s; i += kScoreThreads) {
+        const uint2 q = pts[ck.s + i];
+        const float3 P = deproject(PackedPoint{q.x, __uint_as_float(q.y)}, a.K.cx, a.K.cy, ifx, ify);
+        sp[i] = make_float4(P.x, P.y, P.z, 0.f);
+    }
+    if (threadIdx.x == 0) {                 // region with off[r] <= s < off[r+1]
+        int lo = 0, hi = R;                 // invariant: off[lo] <= s, off[hi] = total > s
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (off[mid] <= ck.s) lo = mid; else hi = mid;
+        }
+        *s_r0 = lo;
+    }
+    __syncthreads();
+    ck.r0 = *s_r0;
+    return true;
+}
+
+// c += (a < b): one FSETP and one predicated IADD (NaN never counts)
+PM_DEVINL void count_lt(int& c, float a, float b) {
+    asm("{\n.reg .pred p;\nsetp.lt.f32 p, %1, %2;\n@p add.s32 %0, %0, 1;\n}" : "+r"(c) : "f"(a), "f"(b));
+}
+
+// The hot loop (Alg. 2 ℓ9-13).  grid = (ceil(W*H / kChunk), B).  Each thread
+// holds kHB hypothesis planes in registers and scores two points per step:
+// 3 FFMA + FSETP + predicated IADD per evaluation.
 template <bool WITH_ERR>
 __global__ void __launch_bounds__(kScoreThreads)
 ransac_score_kernel(RansacWorkspace ws, RansacArgs a) {
     __shared__ float4 sp[kChunk];
     __shared__ int s_r0;
     const size_t f = blockIdx.y;
+    Chunk ck;
+    if (!stage_chunk(ws, a, f, sp, &s_r0, ck)) return;
     const int R = ws.R, HP = ws.n_hyp_pad;
     const int32_t* off = ws.region_off + f * (size_t)(R + 1);
-    const int total = off[R];
-    const int s = blockIdx.x * kChunk;
-    if (s >= total) return;
-    const int e = min(s + kChunk, total);
-    const uint2* pts = ws.points + f * (size_t)ws.W * ws.H;
-    const float ifx = 1.0f / a.K.fx, ify = 1.0f / a.K.fy;
-    for (int i = threadIdx.x; i < e - s; i += kScoreThreads) {
-        const uint2 q = pts[s + i];
-        const float3 P = deproject(PackedPoint{q.x, __uint_as_float(q.y)}, a.K.cx, a.K.cy, ifx, ify);
-        sp[i] = make_float4(P.x, P.y, P.z, 0.f);
-    }
-    if (threadIdx.x == 0) {                 // first region with off[r] <= s < off[r+1]
-        int lo = 0, hi = R;                 // invariant: off[lo] <= s, off[hi] = total > s
-        while (hi - lo > 1) {
-            const int mid = (lo + hi) >> 1;
-            if (off[mid] <= s) lo = mid; else hi = mid;
-        }
-        s_r0 = lo;
-    }
-    __syncthreads();
     const float tau = a.tau;
     const int lane = threadIdx.x & 31;
-    for (int r = s_r0; r < R && off[r] < e; ++r) {
-        const int lo = max(s, off[r]) - s, hi = min(e, off[r + 1]) - s;
+    for (int r = ck.r0; r < R && off[r] < ck.e; ++r) {
+        const int lo = max(ck.s, off[r]) - ck.s, hi = min(ck.e, off[r + 1]) - ck.s;
         if (hi <= lo) continue;
         const float4* planes = ws.planes + (f * R + r) * HP;
         int32_t* counts = ws.counts + (f * R + r) * HP;
@@ -159,13 +191,25 @@ ransac_score_kernel(RansacWorkspace ws, RansacArgs a) {
             uint64_t eq[kHB];
 #pragma unroll
             for (int j = 0; j < kHB; ++j) { c[j] = 0; eq[j] = 0; }
-            for (int i = lo + threadIdx.x; i < hi; i += kScoreThreads) {
+            int i = lo + threadIdx.x;
+            if (!WITH_ERR) {
+                for (; i + kScoreThreads < hi; i += 2 * kScoreThreads) {
+                    const float4 p0 = sp[i], p1 = sp[i + kScoreThreads];
+                    const float3 P0 = make_float3(p0.x, p0.y, p0.z), P1 = make_float3(p1.x, p1.y, p1.z);
+#pragma unroll
+                    for (int j = 0; j < kHB; ++j) {
+                        count_lt(c[j], plane_dist(pl[j], P0), tau);
+                        count_lt(c[j], plane_dist(pl[j], P1), tau);
+                    }
+                }
+            }
+            for (; i < hi; i += kScoreThreads) {
                 const float4 p4 = sp[i];
                 const float3 P = make_float3(p4.x, p4.y, p4.z);
 #pragma unroll
                 for (int j = 0; j < kHB; ++j) {
                     const float dist = plane_dist(pl[j], P);
-                    c[j] += dist < tau ? 1 : 0;
+                    count_lt(c[j], dist, tau);
                     if (WITH_ERR) eq[j] += __float2ull_rn(__fmul_rn(fminf(dist, 64.0f), 16777216.0f));
                 }
             }
@@ -185,14 +229,34 @@ ransac_score_kernel(RansacWorkspace ws, RansacArgs a) {
     }
 }
 
-// ---- fp64 refit helpers
-struct Sums {
-    double s[3];     // sum of q = p - o over inliers
-    double m[6];     // sum of q q^T (xx, xy, xz, yy, yz, zz)
-    int n;
-    unsigned long long err;
+// ---- ℓ14-17 selection: argmax count (or argmin error), ties -> lowest h.
+// Every caller evaluates the same order-free rule, so results agree.
+struct Best {
+    unsigned long long score;   // 0 = no valid hypothesis
+    int h;
 };
+PM_DEVINL void best_merge(Best& b, unsigned long long sc, int h) {
+    if (sc > b.score || (sc == b.score && h < b.h)) { b.score = sc; b.h = h; }
+}
+PM_DEVINL unsigned long long hyp_score(int select, int32_t c, uint64_t e) {
+    if (c < 0) return 0ull;
+    return select == PM_SELECT_ERROR ? ~(unsigned long long)e : (unsigned long long)(c + 1);
+}
+// warp-cooperative: all lanes return the result
+PM_DEVINL Best warp_select(const int32_t* counts, const uint64_t* errq, int NH, int select) {
+    Best b{0ull, 0x7FFFFFFF};
+    for (int h = (int)(threadIdx.x & 31); h < NH; h += 32) best_merge(b, hyp_score(select, counts[h], errq[h]), h);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long sc = __shfl_xor_sync(kFull, b.score, o);
+        const int h = __shfl_xor_sync(kFull, b.h, o);
+        best_merge(b, sc, h);
+    }
+    return b;
+}
 
+// ---- fp64 refit: shifted moments of the winner's inliers, per (region,
+// chunk) slot, reduced in a fixed order (deterministic).
 PM_DEVINL void sums_add(Sums& a, const Sums& b) {
 #pragma unroll
     for (int k = 0; k < 3; ++k) a.s[k] += b.s[k];
@@ -210,7 +274,60 @@ PM_DEVINL Sums sums_shfl_xor(const Sums& a, int o) {
     for (int k = 0; k < 6; ++k) b.m[k] = __shfl_xor_sync(kFull, a.m[k], o);
     b.n = __shfl_xor_sync(kFull, a.n, o);
     b.err = __shfl_xor_sync(kFull, a.err, o);
+    b.pad = 0;
     return b;
+}
+
+// grid = score's grid.  For every region segment of the chunk: select the
+// winner, recount its inliers with the same f32 arithmetic, accumulate
+// moments, write slot (chunk + region).
+__global__ void __launch_bounds__(kScoreThreads)
+ransac_refit_kernel(RansacWorkspace ws, RansacArgs a) {
+    __shared__ float4 sp[kChunk];
+    __shared__ int s_r0;
+    __shared__ Sums s_part[kScoreThreads / 32];
+    const size_t f = blockIdx.y;
+    Chunk ck;
+    if (!stage_chunk(ws, a, f, sp, &s_r0, ck)) return;
+    const int R = ws.R, HP = ws.n_hyp_pad;
+    const int32_t* off = ws.region_off + f * (size_t)(R + 1);
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const uint2* pts = ws.points + f * (size_t)ws.W * ws.H;
+    const float ifx = 1.0f / a.K.fx, ify = 1.0f / a.K.fy;
+    for (int r = ck.r0; r < R && off[r] < ck.e; ++r) {
+        const int lo = max(ck.s, off[r]) - ck.s, hi = min(ck.e, off[r + 1]) - ck.s;
+        if (hi <= lo || off[r + 1] - off[r] < 3) continue;
+        const Best b = warp_select(ws.counts + (f * R + r) * HP, ws.errq + (f * R + r) * HP, ws.n_hyp, a.select);
+        if (b.score == 0ull) continue;                        // degenerate region
+        const float4 pl = ws.planes[(f * R + r) * HP + b.h];
+        const uint2 q0 = pts[off[r]];
+        const float3 o3 = deproject(PackedPoint{q0.x, __uint_as_float(q0.y)}, a.K.cx, a.K.cy, ifx, ify);
+        const double ox = o3.x, oy = o3.y, oz = o3.z;
+        Sums acc = {};
+        for (int i = lo + threadIdx.x; i < hi; i += kScoreThreads) {
+            const float4 p4 = sp[i];
+            const float3 P = make_float3(p4.x, p4.y, p4.z);
+            const float dist = plane_dist(pl, P);
+            acc.err += __float2ull_rn(__fmul_rn(fminf(dist, 64.0f), 16777216.0f));
+            if (dist < a.tau) {
+                const double x = (double)P.x - ox, y = (double)P.y - oy, z = (double)P.z - oz;
+                acc.s[0] += x; acc.s[1] += y; acc.s[2] += z;
+                acc.m[0] = fma(x, x, acc.m[0]); acc.m[1] = fma(x, y, acc.m[1]); acc.m[2] = fma(x, z, acc.m[2]);
+                acc.m[3] = fma(y, y, acc.m[3]); acc.m[4] = fma(y, z, acc.m[4]); acc.m[5] = fma(z, z, acc.m[5]);
+                acc.n += 1;
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) sums_add(acc, sums_shfl_xor(acc, o));
+        if (lane == 0) s_part[w] = acc;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            Sums t = s_part[0];
+            for (int k = 1; k < kScoreThreads / 32; ++k) sums_add(t, s_part[k]);
+            ws.slots[f * (size_t)ws.n_slots + blockIdx.x + r] = t;
+        }
+        __syncthreads();
+    }
 }
 
 // Smallest-eigenvalue eigenvector of a symmetric 3x3 (double) by cyclic
@@ -254,95 +371,43 @@ PM_DEVINL void smallest_eigvec(double A[3][3], double out[3]) {
     out[2] = V[2][m] / nn;
 }
 
-__global__ void __launch_bounds__(kSelectThreads)
-ransac_select_kernel(RansacWorkspace ws, RansacArgs a, pm_plane* __restrict__ planes_out) {
-    __shared__ unsigned long long s_key[kSelectThreads / 32];
-    __shared__ int s_h[kSelectThreads / 32];
-    __shared__ Sums s_sums[kSelectThreads / 32];
-    const int r = blockIdx.x;
+// One thread per (frame, region): selection, slot reduction in chunk order,
+// eigen-solve, gate (ℓ19), pm_plane output.
+constexpr int kFinalThreads = 128;
+__global__ void __launch_bounds__(kFinalThreads)
+ransac_finalize_kernel(RansacWorkspace ws, RansacArgs a, pm_plane* __restrict__ planes_out) {
+    const int r = blockIdx.x * kFinalThreads + threadIdx.x;
     const size_t f = blockIdx.y;
     const int R = ws.R, HP = ws.n_hyp_pad, NH = ws.n_hyp;
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    if (r >= R) return;
     const int32_t* off = ws.region_off + f * (size_t)(R + 1);
     const int base = off[r];
     const int n = off[r + 1] - base;
     const int32_t* counts = ws.counts + (f * R + r) * HP;
     const uint64_t* errq = ws.errq + (f * R + r) * HP;
-    pm_plane* out = planes_out + f * R + r;
     if (a.counts_out)
-        for (int h = threadIdx.x; h < NH; h += kSelectThreads) a.counts_out[(f * R + r) * NH + h] = counts[h];
+        for (int h = 0; h < NH; ++h) a.counts_out[(f * R + r) * NH + h] = counts[h];
     if (a.errq_out)
-        for (int h = threadIdx.x; h < NH; h += kSelectThreads) a.errq_out[(f * R + r) * NH + h] = errq[h];
-
+        for (int h = 0; h < NH; ++h) a.errq_out[(f * R + r) * NH + h] = errq[h];
     pm_plane res;
     for (int k = 0; k < 3; ++k) { res.n[k] = 0.f; res.centroid[k] = 0.f; }
     res.d = 0.f; res.inliers = 0; res.n_points = n; res.best_hyp = -1; res.sum_dist = 0.f;
-    if (n < 3) {
-        res.status = PM_PLANE_TOO_FEW;
-        if (threadIdx.x == 0) *out = res;
-        return;
-    }
-    // ---- ℓ14-17: selection.  score orders "better" hypotheses higher (0 =
-    // invalid): count + 1 (argmax inliers), or ~errq (argmin error, as printed);
-    // ties go to the lowest h.
-    unsigned long long best_p = 0ull;
-    int best_h = 0x7FFFFFFF;
-    for (int h = threadIdx.x; h < NH; h += kSelectThreads) {
-        const int c = counts[h];
-        if (c < 0) continue;
-        const unsigned long long sc = a.select == PM_SELECT_ERROR ? ~(unsigned long long)errq[h]
-                                                                  : (unsigned long long)(c + 1);
-        if (sc > best_p || (sc == best_p && h < best_h)) { best_p = sc; best_h = h; }
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        const unsigned long long op = __shfl_xor_sync(kFull, best_p, o);
-        const int oh = __shfl_xor_sync(kFull, best_h, o);
-        if (op > best_p || (op == best_p && oh < best_h)) { best_p = op; best_h = oh; }
-    }
-    if (lane == 0) { s_key[w] = best_p; s_h[w] = best_h; }
-    __syncthreads();
-    best_p = s_key[0];
-    best_h = s_h[0];
-    for (int k = 1; k < kSelectThreads / 32; ++k)
-        if (s_key[k] > best_p || (s_key[k] == best_p && s_h[k] < best_h)) { best_p = s_key[k]; best_h = s_h[k]; }
-    if (best_p == 0ull) {
-        res.status = PM_PLANE_DEGENERATE;
-        if (threadIdx.x == 0) *out = res;
-        return;
-    }
-    const int best = best_h;
+    pm_plane* out = planes_out + f * R + r;
+    if (n < 3) { res.status = PM_PLANE_TOO_FEW; *out = res; return; }
+    Best b{0ull, 0x7FFFFFFF};
+    for (int h = 0; h < NH; ++h) best_merge(b, hyp_score(a.select, counts[h], errq[h]), h);
+    if (b.score == 0ull) { res.status = PM_PLANE_DEGENERATE; *out = res; return; }
+    const int best = b.h;
     const float4 pl = ws.planes[(f * R + r) * HP + best];
+    // slots of this region: chunks c0..c1 -> slot c + r (ascending order)
+    const int c0 = base / kChunk, c1 = (base + n - 1) / kChunk;
+    const Sums* sl = ws.slots + f * (size_t)ws.n_slots;
+    Sums t = sl[c0 + r];
+    for (int c = c0 + 1; c <= c1; ++c) sums_add(t, sl[c + r]);
     const uint2* pts = ws.points + f * (size_t)ws.W * ws.H + base;
     const float ifx = 1.0f / a.K.fx, ify = 1.0f / a.K.fy;
-
-    // ---- refit: shifted fp64 moments of the winner's inliers (one pass)
     const uint2 q0 = pts[0];
     const float3 o3 = deproject(PackedPoint{q0.x, __uint_as_float(q0.y)}, a.K.cx, a.K.cy, ifx, ify);
-    const double ox = o3.x, oy = o3.y, oz = o3.z;
-    Sums acc = {};
-    for (int i = threadIdx.x; i < n; i += kSelectThreads) {
-        const uint2 q = pts[i];
-        const float3 P = deproject(PackedPoint{q.x, __uint_as_float(q.y)}, a.K.cx, a.K.cy, ifx, ify);
-        const float dist = plane_dist(pl, P);
-        acc.err += __float2ull_rn(__fmul_rn(fminf(dist, 64.0f), 16777216.0f));
-        if (dist < a.tau) {
-            const double x = (double)P.x - ox, y = (double)P.y - oy, z = (double)P.z - oz;
-            acc.s[0] += x; acc.s[1] += y; acc.s[2] += z;
-            acc.m[0] += x * x; acc.m[1] += x * y; acc.m[2] += x * z;
-            acc.m[3] += y * y; acc.m[4] += y * z; acc.m[5] += z * z;
-            acc.n += 1;
-        }
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) sums_add(acc, sums_shfl_xor(acc, o));
-    if (lane == 0) s_sums[w] = acc;
-    __syncthreads();
-    if (threadIdx.x != 0) return;
-    Sums t = s_sums[0];
-    for (int k = 1; k < kSelectThreads / 32; ++k) sums_add(t, s_sums[k]);
-
-    const int inl = counts[best];
     double nv[3], cen[3], dd;
     if (t.n >= 3) {
         const double inv = 1.0 / t.n;
@@ -352,11 +417,13 @@ ransac_select_kernel(RansacWorkspace ws, RansacArgs a, pm_plane* __restrict__ pl
         A[1][1] = t.m[3] - t.n * my * my; A[1][2] = t.m[4] - t.n * my * mz; A[2][2] = t.m[5] - t.n * mz * mz;
         A[1][0] = A[0][1]; A[2][0] = A[0][2]; A[2][1] = A[1][2];
         smallest_eigvec(A, nv);
-        cen[0] = ox + mx; cen[1] = oy + my; cen[2] = oz + mz;
+        cen[0] = (double)o3.x + mx; cen[1] = (double)o3.y + my; cen[2] = (double)o3.z + mz;
+        dd = -(nv[0] * cen[0] + nv[1] * cen[1] + nv[2] * cen[2]);
     } else {
         // refit impossible (tau below rounding): keep the 3-point model,
         // centroid = mean of its three sample points (Q19)
-        const SampleIdx s = sample(a.sampler, (uint32_t)best, (uint32_t)r, a.first_frame + (uint32_t)f, a.seed, (uint32_t)n);
+        const SampleIdx s = sample(a.sampler, (uint32_t)best, (uint32_t)r, a.first_frame + (uint32_t)f, a.seed,
+                                   (uint32_t)n);
         const uint32_t id[3] = {s.i0, s.i1, s.i2};
         cen[0] = cen[1] = cen[2] = 0.0;
         for (int k = 0; k < 3; ++k) {
@@ -366,15 +433,14 @@ ransac_select_kernel(RansacWorkspace ws, RansacArgs a, pm_plane* __restrict__ pl
         }
         for (int k = 0; k < 3; ++k) cen[k] /= 3.0;
         nv[0] = pl.x; nv[1] = pl.y; nv[2] = pl.z;
+        dd = pl.w;
     }
-    dd = -(nv[0] * cen[0] + nv[1] * cen[1] + nv[2] * cen[2]);
-    if (t.n < 3) dd = pl.w;
     if (dd < 0.0) { nv[0] = -nv[0]; nv[1] = -nv[1]; nv[2] = -nv[2]; dd = -dd; }
     for (int k = 0; k < 3; ++k) { res.n[k] = (float)nv[k]; res.centroid[k] = (float)cen[k]; }
     res.d = (float)dd;
-    res.inliers = inl;
+    res.inliers = counts[best];
     res.best_hyp = best;
-    res.status = (10ll * inl > 9ll * n) ? PM_PLANE_OK : PM_PLANE_REJECTED;   // ℓ19
+    res.status = (10ll * counts[best] > 9ll * n) ? PM_PLANE_OK : PM_PLANE_REJECTED;   // ℓ19
     res.sum_dist = (float)((double)t.err * (1.0 / 16777216.0));
     *out = res;
 }
@@ -392,6 +458,7 @@ RansacWorkspace ransac_workspace_layout(void* base, int W, int H, int R, int n_h
     while (st < 4 * R && st < (1 << 24)) st <<= 1;      // hist entries <= ~W*H/4 per frame
     ws.sub_tile = st;
     ws.n_sub = (int)((WH + st - 1) / st);
+    ws.n_slots = (int)((WH + kChunk - 1) / kChunk) + R;
     const size_t Rm = R > 0 ? R : 1;
     size_t o = 0;
     char* p = (char*)base;
@@ -403,6 +470,7 @@ RansacWorkspace ransac_workspace_layout(void* base, int W, int H, int R, int n_h
     ws.planes = (float4*)take(sizeof(float4) * B * Rm * ws.n_hyp_pad);
     ws.counts = (int32_t*)take(sizeof(int32_t) * B * Rm * ws.n_hyp_pad);
     ws.errq = (uint64_t*)take(sizeof(uint64_t) * B * Rm * ws.n_hyp_pad);
+    ws.slots = (Sums*)take(sizeof(Sums) * B * (size_t)ws.n_slots);
     ws.total_bytes = o;
     return ws;
 }
@@ -412,12 +480,14 @@ cudaError_t ransac_run(const RansacWorkspace& ws, const RansacArgs& a, pm_plane*
     const bool need_err = a.select == PM_SELECT_ERROR || a.errq_out != nullptr;
     const int n_hyp_slots = ws.R * ws.n_hyp_pad;
     ransac_hyp_kernel<<<dim3((n_hyp_slots + 255) / 256, ws.B), 256, 0, stream>>>(ws, a, need_err ? 1 : 0);
-    const dim3 g_score((unsigned)(((size_t)ws.W * ws.H + kChunk - 1) / kChunk), ws.B);
+    const dim3 g_chunks((unsigned)(((size_t)ws.W * ws.H + kChunk - 1) / kChunk), ws.B);
     if (need_err)
-        ransac_score_kernel<true><<<g_score, kScoreThreads, 0, stream>>>(ws, a);
+        ransac_score_kernel<true><<<g_chunks, kScoreThreads, 0, stream>>>(ws, a);
     else
-        ransac_score_kernel<false><<<g_score, kScoreThreads, 0, stream>>>(ws, a);
-    ransac_select_kernel<<<dim3(ws.R, ws.B), kSelectThreads, 0, stream>>>(ws, a, planes);
+        ransac_score_kernel<false><<<g_chunks, kScoreThreads, 0, stream>>>(ws, a);
+    ransac_refit_kernel<<<g_chunks, kScoreThreads, 0, stream>>>(ws, a);
+    ransac_finalize_kernel<<<dim3((ws.R + kFinalThreads - 1) / kFinalThreads, ws.B), kFinalThreads, 0, stream>>>(
+        ws, a, planes);
     return cudaGetLastError();
 }
 
