@@ -17,6 +17,7 @@
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 #include "internal.h"
@@ -37,7 +38,8 @@ namespace {
 constexpr unsigned kFull = 0xFFFFFFFFu;
 constexpr int kScoreThreads = 256;
 constexpr int kChunk = 2048;          // points per scoring CTA
-constexpr int kHB = 8;                // hypotheses per register block
+constexpr int kHB = 8;                // hypothesis array padding
+constexpr int kRefitChunk = 8192;     // points per refit CTA
 
 struct SampleIdx { uint32_t i0, i1, i2; bool ok; };
 
@@ -162,69 +164,80 @@ PM_DEVINL void count_lt(int& c, float a, float b) {
     asm("{\n.reg .pred p;\nsetp.lt.f32 p, %1, %2;\n@p add.s32 %0, %0, 1;\n}" : "+r"(c) : "f"(a), "f"(b));
 }
 
-// The hot loop (Alg. 2 ℓ9-13).  grid = (ceil(W*H / kChunk), B).  Each thread
-// holds kHB hypothesis planes in registers and scores two points per step:
-// 3 FFMA + FSETP + predicated IADD per evaluation.
-template <bool WITH_ERR>
+// The hot loop (Alg. 2 ℓ9-13).  grid = (ceil(W*H / kChunk), B).  The CTA's
+// threads form G = 256 / L groups of L lanes; lane l of every group holds
+// hypotheses l, l + L, ..., l + (K-1) L of the current region in registers;
+// group g walks points g, g + G, ... of the segment, each point a broadcast
+// shared load.  An evaluation costs 3 FFMA + FSETP + a predicated IADD; the
+// only reduction is one shared-memory sum over the G groups per segment and
+// one integer atomic per hypothesis (exact and order-free).
+template <int K, bool WITH_ERR>
 __global__ void __launch_bounds__(kScoreThreads)
-ransac_score_kernel(RansacWorkspace ws, RansacArgs a) {
+ransac_score_kernel(RansacWorkspace ws, RansacArgs a, int L) {
     __shared__ float4 sp[kChunk];
     __shared__ int s_r0;
+    constexpr bool kSmemReduce = K <= 8;     // K = 16 would exceed the 48 KB static limit
+    __shared__ int s_cnt[kScoreThreads * (kSmemReduce ? K : 1)];
     const size_t f = blockIdx.y;
     Chunk ck;
     if (!stage_chunk(ws, a, f, sp, &s_r0, ck)) return;
-    const int R = ws.R, HP = ws.n_hyp_pad;
+    const int R = ws.R, HP = ws.n_hyp_pad, NH = ws.n_hyp;
+    const int G = kScoreThreads / L;
+    const int g = threadIdx.x / L, l = threadIdx.x - g * L;
     const int32_t* off = ws.region_off + f * (size_t)(R + 1);
     const float tau = a.tau;
-    const int lane = threadIdx.x & 31;
+    const float4 nan4 = make_float4(__int_as_float(0x7FC00000), 0.f, 0.f, 0.f);
     for (int r = ck.r0; r < R && off[r] < ck.e; ++r) {
         const int lo = max(ck.s, off[r]) - ck.s, hi = min(ck.e, off[r + 1]) - ck.s;
-        if (hi <= lo) continue;
+        if (hi <= lo || off[r + 1] - off[r] < 3) continue;
         const float4* planes = ws.planes + (f * R + r) * HP;
         int32_t* counts = ws.counts + (f * R + r) * HP;
         uint64_t* errq = ws.errq + (f * R + r) * HP;
-        for (int h0 = 0; h0 < ws.n_hyp; h0 += kHB) {
-            float4 pl[kHB];
+        float4 pl[K];
+        int c[K];
+        uint64_t eq[K];
 #pragma unroll
-            for (int j = 0; j < kHB; ++j) pl[j] = __ldg(planes + h0 + j);
-            int c[kHB];
-            uint64_t eq[kHB];
+        for (int k = 0; k < K; ++k) {
+            const int h = l + k * L;
+            pl[k] = h < NH ? __ldg(planes + h) : nan4;
+            c[k] = 0;
+            eq[k] = 0;
+        }
+#pragma unroll 4
+        for (int i = lo + g; i < hi; i += G) {
+            const float4 p4 = sp[i];
+            const float3 P = make_float3(p4.x, p4.y, p4.z);
 #pragma unroll
-            for (int j = 0; j < kHB; ++j) { c[j] = 0; eq[j] = 0; }
-            int i = lo + threadIdx.x;
-            if (!WITH_ERR) {
-                for (; i + kScoreThreads < hi; i += 2 * kScoreThreads) {
-                    const float4 p0 = sp[i], p1 = sp[i + kScoreThreads];
-                    const float3 P0 = make_float3(p0.x, p0.y, p0.z), P1 = make_float3(p1.x, p1.y, p1.z);
-#pragma unroll
-                    for (int j = 0; j < kHB; ++j) {
-                        count_lt(c[j], plane_dist(pl[j], P0), tau);
-                        count_lt(c[j], plane_dist(pl[j], P1), tau);
-                    }
-                }
+            for (int k = 0; k < K; ++k) {
+                const float dist = plane_dist(pl[k], P);
+                count_lt(c[k], dist, tau);
+                if (WITH_ERR) eq[k] += __float2ull_rn(__fmul_rn(fminf(dist, 64.0f), 16777216.0f));
             }
-            for (; i < hi; i += kScoreThreads) {
-                const float4 p4 = sp[i];
-                const float3 P = make_float3(p4.x, p4.y, p4.z);
+        }
+        if (WITH_ERR) {
 #pragma unroll
-                for (int j = 0; j < kHB; ++j) {
-                    const float dist = plane_dist(pl[j], P);
-                    count_lt(c[j], dist, tau);
-                    if (WITH_ERR) eq[j] += __float2ull_rn(__fmul_rn(fminf(dist, 64.0f), 16777216.0f));
-                }
+            for (int k = 0; k < K; ++k) {
+                const int h = l + k * L;
+                if (h < NH && eq[k] > 0 && !isnan(pl[k].x))
+                    atomicAdd((unsigned long long*)(errq + h), (unsigned long long)eq[k]);
             }
+        }
+        if (G == 1 || !kSmemReduce) {
 #pragma unroll
-            for (int j = 0; j < kHB; ++j) {
-                const int cw = __reduce_add_sync(kFull, c[j]);
-                if (lane == 0 && cw > 0) atomicAdd(counts + h0 + j, cw);
-                if (WITH_ERR) {
-                    uint64_t ew = eq[j];
-#pragma unroll
-                    for (int o = 16; o > 0; o >>= 1) ew += __shfl_xor_sync(kFull, ew, o);
-                    if (lane == 0 && ew > 0 && !isnan(pl[j].x))
-                        atomicAdd((unsigned long long*)(errq + h0 + j), (unsigned long long)ew);
-                }
+            for (int k = 0; k < K; ++k) {
+                const int h = l + k * L;
+                if (h < NH && c[k] > 0) atomicAdd(counts + h, c[k]);
             }
+        } else {
+#pragma unroll
+            for (int k = 0; k < K; ++k) s_cnt[g * (L * K) + k * L + l] = c[k];
+            __syncthreads();
+            for (int h = threadIdx.x; h < L * K; h += kScoreThreads) {
+                int sum = 0;
+                for (int q = 0; q < G; ++q) sum += s_cnt[q * (L * K) + h];
+                if (h < NH && sum > 0) atomicAdd(counts + h, sum);
+            }
+            __syncthreads();
         }
     }
 }
@@ -278,53 +291,70 @@ PM_DEVINL Sums sums_shfl_xor(const Sums& a, int o) {
     return b;
 }
 
-// grid = score's grid.  For every region segment of the chunk: select the
-// winner, recount its inliers with the same f32 arithmetic, accumulate
-// moments, write slot (chunk + region).
+// grid = (ceil(W*H / kRefitChunk), B).  For every region segment of the
+// chunk: select the winner (warp 0), recount its inliers with the same f32
+// arithmetic, accumulate fp64 moments, write slot (chunk + region).
 __global__ void __launch_bounds__(kScoreThreads)
 ransac_refit_kernel(RansacWorkspace ws, RansacArgs a) {
-    __shared__ float4 sp[kChunk];
-    __shared__ int s_r0;
     __shared__ Sums s_part[kScoreThreads / 32];
+    __shared__ int s_best;
+    __shared__ int s_r0;
     const size_t f = blockIdx.y;
-    Chunk ck;
-    if (!stage_chunk(ws, a, f, sp, &s_r0, ck)) return;
     const int R = ws.R, HP = ws.n_hyp_pad;
     const int32_t* off = ws.region_off + f * (size_t)(R + 1);
+    const int total = off[R];
+    const int cs = blockIdx.x * kRefitChunk;
+    if (cs >= total) return;
+    const int ce = min(cs + kRefitChunk, total);
+    if (threadIdx.x == 0) {
+        int lo = 0, hi = R;
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (off[mid] <= cs) lo = mid; else hi = mid;
+        }
+        s_r0 = lo;
+    }
+    __syncthreads();
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const uint2* pts = ws.points + f * (size_t)ws.W * ws.H;
     const float ifx = 1.0f / a.K.fx, ify = 1.0f / a.K.fy;
-    for (int r = ck.r0; r < R && off[r] < ck.e; ++r) {
-        const int lo = max(ck.s, off[r]) - ck.s, hi = min(ck.e, off[r + 1]) - ck.s;
+    for (int r = s_r0; r < R && off[r] < ce; ++r) {
+        const int lo = max(cs, off[r]), hi = min(ce, off[r + 1]);
         if (hi <= lo || off[r + 1] - off[r] < 3) continue;
-        const Best b = warp_select(ws.counts + (f * R + r) * HP, ws.errq + (f * R + r) * HP, ws.n_hyp, a.select);
-        if (b.score == 0ull) continue;                        // degenerate region
-        const float4 pl = ws.planes[(f * R + r) * HP + b.h];
-        const uint2 q0 = pts[off[r]];
-        const float3 o3 = deproject(PackedPoint{q0.x, __uint_as_float(q0.y)}, a.K.cx, a.K.cy, ifx, ify);
-        const double ox = o3.x, oy = o3.y, oz = o3.z;
-        Sums acc = {};
-        for (int i = lo + threadIdx.x; i < hi; i += kScoreThreads) {
-            const float4 p4 = sp[i];
-            const float3 P = make_float3(p4.x, p4.y, p4.z);
-            const float dist = plane_dist(pl, P);
-            acc.err += __float2ull_rn(__fmul_rn(fminf(dist, 64.0f), 16777216.0f));
-            if (dist < a.tau) {
-                const double x = (double)P.x - ox, y = (double)P.y - oy, z = (double)P.z - oz;
-                acc.s[0] += x; acc.s[1] += y; acc.s[2] += z;
-                acc.m[0] = fma(x, x, acc.m[0]); acc.m[1] = fma(x, y, acc.m[1]); acc.m[2] = fma(x, z, acc.m[2]);
-                acc.m[3] = fma(y, y, acc.m[3]); acc.m[4] = fma(y, z, acc.m[4]); acc.m[5] = fma(z, z, acc.m[5]);
-                acc.n += 1;
-            }
+        if (w == 0) {
+            const Best b = warp_select(ws.counts + (f * R + r) * HP, ws.errq + (f * R + r) * HP, ws.n_hyp, a.select);
+            if (lane == 0) s_best = b.score == 0ull ? -1 : b.h;
         }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) sums_add(acc, sums_shfl_xor(acc, o));
-        if (lane == 0) s_part[w] = acc;
         __syncthreads();
-        if (threadIdx.x == 0) {
-            Sums t = s_part[0];
-            for (int k = 1; k < kScoreThreads / 32; ++k) sums_add(t, s_part[k]);
-            ws.slots[f * (size_t)ws.n_slots + blockIdx.x + r] = t;
+        const int best = s_best;
+        if (best >= 0) {
+            const float4 pl = ws.planes[(f * R + r) * HP + best];
+            const uint2 q0 = pts[off[r]];
+            const float3 o3 = deproject(PackedPoint{q0.x, __uint_as_float(q0.y)}, a.K.cx, a.K.cy, ifx, ify);
+            const double ox = o3.x, oy = o3.y, oz = o3.z;
+            Sums acc = {};
+            for (int i = lo + threadIdx.x; i < hi; i += kScoreThreads) {
+                const uint2 q = pts[i];
+                const float3 P = deproject(PackedPoint{q.x, __uint_as_float(q.y)}, a.K.cx, a.K.cy, ifx, ify);
+                const float dist = plane_dist(pl, P);
+                acc.err += __float2ull_rn(__fmul_rn(fminf(dist, 64.0f), 16777216.0f));
+                if (dist < a.tau) {
+                    const double x = (double)P.x - ox, y = (double)P.y - oy, z = (double)P.z - oz;
+                    acc.s[0] += x; acc.s[1] += y; acc.s[2] += z;
+                    acc.m[0] = fma(x, x, acc.m[0]); acc.m[1] = fma(x, y, acc.m[1]); acc.m[2] = fma(x, z, acc.m[2]);
+                    acc.m[3] = fma(y, y, acc.m[3]); acc.m[4] = fma(y, z, acc.m[4]); acc.m[5] = fma(z, z, acc.m[5]);
+                    acc.n += 1;
+                }
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) sums_add(acc, sums_shfl_xor(acc, o));
+            if (lane == 0) s_part[w] = acc;
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                Sums t = s_part[0];
+                for (int k = 1; k < kScoreThreads / 32; ++k) sums_add(t, s_part[k]);
+                ws.slots[f * (size_t)ws.n_slots + blockIdx.x + r] = t;
+            }
         }
         __syncthreads();
     }
@@ -400,7 +430,7 @@ ransac_finalize_kernel(RansacWorkspace ws, RansacArgs a, pm_plane* __restrict__ 
     const int best = b.h;
     const float4 pl = ws.planes[(f * R + r) * HP + best];
     // slots of this region: chunks c0..c1 -> slot c + r (ascending order)
-    const int c0 = base / kChunk, c1 = (base + n - 1) / kChunk;
+    const int c0 = base / kRefitChunk, c1 = (base + n - 1) / kRefitChunk;
     const Sums* sl = ws.slots + f * (size_t)ws.n_slots;
     Sums t = sl[c0 + r];
     for (int c = c0 + 1; c <= c1; ++c) sums_add(t, sl[c + r]);
@@ -458,7 +488,7 @@ RansacWorkspace ransac_workspace_layout(void* base, int W, int H, int R, int n_h
     while (st < 4 * R && st < (1 << 24)) st <<= 1;      // hist entries <= ~W*H/4 per frame
     ws.sub_tile = st;
     ws.n_sub = (int)((WH + st - 1) / st);
-    ws.n_slots = (int)((WH + kChunk - 1) / kChunk) + R;
+    ws.n_slots = (int)((WH + kRefitChunk - 1) / kRefitChunk) + R;
     const size_t Rm = R > 0 ? R : 1;
     size_t o = 0;
     char* p = (char*)base;
@@ -481,11 +511,23 @@ cudaError_t ransac_run(const RansacWorkspace& ws, const RansacArgs& a, pm_plane*
     const int n_hyp_slots = ws.R * ws.n_hyp_pad;
     ransac_hyp_kernel<<<dim3((n_hyp_slots + 255) / 256, ws.B), 256, 0, stream>>>(ws, a, need_err ? 1 : 0);
     const dim3 g_chunks((unsigned)(((size_t)ws.W * ws.H + kChunk - 1) / kChunk), ws.B);
-    if (need_err)
-        ransac_score_kernel<true><<<g_chunks, kScoreThreads, 0, stream>>>(ws, a);
-    else
-        ransac_score_kernel<false><<<g_chunks, kScoreThreads, 0, stream>>>(ws, a);
-    ransac_refit_kernel<<<g_chunks, kScoreThreads, 0, stream>>>(ws, a);
+    // K hypotheses per lane, L lanes per group (L * K >= n_hyp): small L
+    // means more points in flight per warp and a cheaper per-point overhead
+    auto pow2ceil = [](int x) { int p = 1; while (p < x) p <<= 1; return p; };
+    int L = pow2ceil((ws.n_hyp + 7) / 8);
+    L = L < 8 ? 8 : (L > 256 ? 256 : L);
+    if (const char* e = getenv("PM_SCORE_LANES")) { const int v = atoi(e); if (v >= 8 && v <= 256 && (v & (v - 1)) == 0) L = v; }
+    int K = pow2ceil((ws.n_hyp + L - 1) / L);
+    if (K > 16) { K = 16; L = pow2ceil((ws.n_hyp + 15) / 16); }
+#define PM_SCORE(KK)                                                                              \
+    if (K == KK) {                                                                                \
+        if (need_err) ransac_score_kernel<KK, true><<<g_chunks, kScoreThreads, 0, stream>>>(ws, a, L);  \
+        else ransac_score_kernel<KK, false><<<g_chunks, kScoreThreads, 0, stream>>>(ws, a, L);         \
+    }
+    PM_SCORE(1) PM_SCORE(2) PM_SCORE(4) PM_SCORE(8) PM_SCORE(16)
+#undef PM_SCORE
+    const dim3 g_refit((unsigned)(((size_t)ws.W * ws.H + kRefitChunk - 1) / kRefitChunk), ws.B);
+    ransac_refit_kernel<<<g_refit, kScoreThreads, 0, stream>>>(ws, a);
     ransac_finalize_kernel<<<dim3((ws.R + kFinalThreads - 1) / kFinalThreads, ws.B), kFinalThreads, 0, stream>>>(
         ws, a, planes);
     return cudaGetLastError();
