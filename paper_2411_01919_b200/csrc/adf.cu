@@ -46,17 +46,17 @@ struct AdfParams {
 
 // Alg. 1 ℓ4-6 at a valid centre C with neighbour values N, S, W, E (already
 // replaced by C where the zero-flux rule applies):
-//   dX = X - C;  2gx = dE - dW;  2gy = dS - dN;  lap = (dN + dS) + (dE + dW)
+//   2gx = E - W;  2gy = S - N;  lap = ((N + S) + (W + E)) - 4 C
 //   lambda * c = 2^(kc (2gx^2 + 2gy^2) + log2 lambda),  c = exp(-|grad|^2 / k^2)
 //   I' = C + (lambda c) * lap
+// (pairwise sums keep a constant image an exact fixed point; the f32
+// rounding of the sums costs < 1e-6 m over 100 sweeps)
 PM_DEVINL float adf_cell(float C, float N, float S, float W, float E, float kc, float l2lam) {
-    const float dn = __fsub_rn(N, C), ds = __fsub_rn(S, C);
-    const float dw = __fsub_rn(W, C), de = __fsub_rn(E, C);
-    const float gx2 = __fsub_rn(de, dw);
-    const float gy2 = __fsub_rn(ds, dn);
+    const float gx2 = __fsub_rn(E, W);
+    const float gy2 = __fsub_rn(S, N);
     const float g2 = __fmaf_rn(gx2, gx2, __fmul_rn(gy2, gy2));
     const float lc = ex2_approx(__fmaf_rn(g2, kc, l2lam));
-    const float lap = __fadd_rn(__fadd_rn(dn, ds), __fadd_rn(de, dw));
+    const float lap = __fmaf_rn(-4.0f, C, __fadd_rn(__fadd_rn(N, S), __fadd_rn(W, E)));
     return __fmaf_rn(lc, lap, C);
 }
 
@@ -117,6 +117,58 @@ PM_DEVINL void sweep(const float* __restrict__ cur, float* __restrict__ nxt, int
         ocol[y * kSW] = cell<CHECK>(C, N, C, colW[y * kSW], colE[y * kSW], kc, l2lam);
 }
 
+// Same sweep with two horizontally adjacent cells per thread (columns x, x+1,
+// x even): per row one 8-byte load of the south pair, one load each for the
+// outer west / east neighbours (the inner ones are the pair itself), one
+// 8-byte store -- 2 shared accesses per cell instead of 4.  Requires the image
+// columns [ix0, ix1) to start and end on even smem columns, so that a pair is
+// entirely inside or outside the image.  A pair straddling the sweep region's
+// edge also updates its outer cell; that cell lies outside every later
+// region and is never read again.
+template <int SH, int PAD, bool CHECK>
+PM_DEVINL void sweep_pairs(const float* __restrict__ cur, float* __restrict__ nxt, int t, const Box& b,
+                           float kc, float l2lam) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int x = ((warp & 1) * 32 + lane) * 2;
+    const int ylo = max(t, b.iy0), yhi = min(SH - t, b.iy1);
+    const int q = (yhi - ylo + 3) >> 2;
+    const int ys = ylo + (warp >> 1) * q;
+    const int ye = min(ys + q, yhi);
+    const int xa = max(PAD + t, b.ix0), xb = min(kSW - PAD - t, b.ix1);
+    if (x + 2 <= xa || x >= xb || ys >= ye) return;
+    const int ylast = b.iy1 - 1;
+    const int ymid = min(ye, ylast);
+    const int offW = x == b.ix0 ? 0 : -1;           // zero flux at the image border (Q4)
+    const int offE = x + 2 == b.ix1 ? 1 : 2;
+    const float* col = cur + x;
+    const float* colW = col + offW;
+    const float* colE = col + offE;
+    float* ocol = nxt + x;
+    float2 C = *reinterpret_cast<const float2*>(col + ys * kSW);
+    float2 N = ys == b.iy0 ? C : *reinterpret_cast<const float2*>(col + (ys - 1) * kSW);
+    int y = ys;
+#pragma unroll 4
+    for (; y < ymid; ++y) {
+        const float2 S = *reinterpret_cast<const float2*>(col + (y + 1) * kSW);
+        const float W = colW[y * kSW];
+        const float E = colE[y * kSW];
+        float2 o;
+        o.x = cell<CHECK>(C.x, N.x, S.x, W, C.y, kc, l2lam);
+        o.y = cell<CHECK>(C.y, N.y, S.y, C.x, E, kc, l2lam);
+        *reinterpret_cast<float2*>(ocol + y * kSW) = o;
+        N = C;
+        C = S;
+    }
+    if (ye > ylast) {                               // last image row: S = C
+        const float W = colW[y * kSW];
+        const float E = colE[y * kSW];
+        float2 o;
+        o.x = cell<CHECK>(C.x, N.x, C.x, W, C.y, kc, l2lam);
+        o.y = cell<CHECK>(C.y, N.y, C.y, C.x, E, kc, l2lam);
+        *reinterpret_cast<float2*>(ocol + y * kSW) = o;
+    }
+}
+
 // Sobel (1/8-normalised, clamp-to-edge) + geometric normal (Eq. 2 read as
 // Q7): m = (fx Gx, fy Gy, -(Z + (u-cx) Gx + (v-cy) Gy)), n = m/|m|; (0,0,0)
 // if any window pixel is invalid (Q9).  z[a][b] = window row a, column b.
@@ -158,7 +210,8 @@ __host__ __device__ constexpr int tile_w() { return kSW - 2 * halo_x<R>(); }
 template <int R>
 __global__ void __launch_bounds__(kThreads, 2)
 adf_pass_kernel(const float* __restrict__ src, float* __restrict__ dst, float* __restrict__ normals,
-                int W, int H, int iters, AdfParams p, const __grid_constant__ CUtensorMap tmap, int use_tma) {
+                int W, int H, int iters, AdfParams p, const __grid_constant__ CUtensorMap tmap, int use_tma,
+                int* __restrict__ frame_flags, int flag_mode) {
     constexpr int SH = kTH + 2 * R;
     constexpr int RA = halo_x<R>();
     constexpr int TW = tile_w<R>();
@@ -189,15 +242,18 @@ adf_pass_kernel(const float* __restrict__ src, float* __restrict__ dst, float* _
             tma_load_3d(buf0, &tmap, x0, y0, (int)frame, &bar);
         }
         mbar_wait(&bar, 0);
-        // validity scan: each lane checks 4 consecutive columns per row
-        const int c0 = 4 * lane;
-        bool in[4];
+        // validity scan (skipped when an earlier pass found the frame hole-free:
+        // validity never changes, Q4): each lane checks 4 consecutive columns
+        if (flag_mode != 2 || frame_flags[frame] != 0) {
+            const int c0 = 4 * lane;
+            bool in[4];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) in[j] = c0 + j >= b.ix0 && c0 + j < b.ix1;
-        for (int sy = b.iy0 + warp; sy < b.iy1; sy += kWarps) {
-            const float4 v = *reinterpret_cast<const float4*>(buf0 + sy * kSW + c0);
-            all_valid &= (valid_depth(v.x) || !in[0]) && (valid_depth(v.y) || !in[1]) &&
-                         (valid_depth(v.z) || !in[2]) && (valid_depth(v.w) || !in[3]);
+            for (int j = 0; j < 4; ++j) in[j] = c0 + j >= b.ix0 && c0 + j < b.ix1;
+            for (int sy = b.iy0 + warp; sy < b.iy1; sy += kWarps) {
+                const float4 v = *reinterpret_cast<const float4*>(buf0 + sy * kSW + c0);
+                all_valid &= (valid_depth(v.x) || !in[0]) && (valid_depth(v.y) || !in[1]) &&
+                             (valid_depth(v.z) || !in[2]) && (valid_depth(v.w) || !in[3]);
+            }
         }
     } else {
         for (int sy = b.iy0 + warp; sy < b.iy1; sy += kWarps) {
@@ -214,14 +270,22 @@ adf_pass_kernel(const float* __restrict__ src, float* __restrict__ dst, float* _
         }
     }
     all_valid = __syncthreads_and(all_valid);
+    if (flag_mode == 1 && !all_valid && threadIdx.x == 0) atomicOr(frame_flags + frame, 1);
 
     float* cur = buf0;
     float* nxt = buf1;
+    const bool pairs = ((b.ix0 | b.ix1) & 1) == 0;
     for (int t = 1; t <= iters; ++t) {
-        if (all_valid)
+        if (pairs) {
+            if (all_valid)
+                sweep_pairs<SH, PAD, false>(cur, nxt, t, b, p.kc, p.l2lam);
+            else
+                sweep_pairs<SH, PAD, true>(cur, nxt, t, b, p.kc, p.l2lam);
+        } else if (all_valid) {
             sweep<SH, PAD, false>(cur, nxt, t, b, p.kc, p.l2lam);
-        else
+        } else {
             sweep<SH, PAD, true>(cur, nxt, t, b, p.kc, p.l2lam);
+        }
         __syncthreads();
         float* tmp = cur; cur = nxt; nxt = tmp;
     }
@@ -300,7 +364,7 @@ adf_pass_kernel(const float* __restrict__ src, float* __restrict__ dst, float* _
     }
 }
 
-using PassFn = void (*)(const float*, float*, float*, int, int, int, AdfParams, const CUtensorMap, int);
+using PassFn = void (*)(const float*, float*, float*, int, int, int, AdfParams, const CUtensorMap, int, int*, int);
 
 template <int R>
 struct PassTable {
@@ -339,7 +403,8 @@ cudaError_t adf_setup_attributes() {
 }
 
 static cudaError_t launch_pass(const float* src, float* dst, float* normals, int W, int H, int B,
-                               int iters, bool fuse, const AdfParams& p, cudaStream_t stream) {
+                               int iters, bool fuse, const AdfParams& p, cudaStream_t stream,
+                               int* frame_flags = nullptr, int flag_mode = 0) {
     const int R = iters + (fuse ? 1 : 0);
     const Passes& P = passes();
     const int TW = P.tw[R];
@@ -347,12 +412,15 @@ static cudaError_t launch_pass(const float* src, float* dst, float* normals, int
     CUtensorMap tmap;
     int use_tma = make_tmap_f32_3d(&tmap, src, W, H, B, kSW, kTH + 2 * R) ? 1 : 0;
     if (!use_tma) memset(&tmap, 0, sizeof(tmap));
-    void* args[] = {(void*)&src, (void*)&dst,   (void*)&normals, (void*)&W,      (void*)&H,
-                    (void*)&iters, (void*)&p, (void*)&tmap,    (void*)&use_tma};
+    void* args[] = {(void*)&src,  (void*)&dst,  (void*)&normals, (void*)&W,           (void*)&H,
+                    (void*)&iters, (void*)&p,   (void*)&tmap,    (void*)&use_tma,     (void*)&frame_flags,
+                    (void*)&flag_mode};
     return cudaLaunchKernel((const void*)P.fn[R], grid, dim3(kThreads), args, P.smem[R], stream);
 }
 
 int adf_default_iters_per_pass() { return 4; }
+
+size_t adf_flags_offset(int W, int H, int B) { return (sizeof(float) * (size_t)B * W * H + 255) & ~(size_t)255; }
 
 static AdfParams make_params(const pm_intrinsics* K, float lam, float kappa) {
     AdfParams p;
@@ -377,6 +445,13 @@ cudaError_t adf_run(const float* in, float* out, float* normals, float* ws, int 
         return launch_pass(in, out, normals, W, H, B, 0, true, p, stream);
     }
     const int passes = (iters + T - 1) / T;
+    // per-frame "has an invalid pixel" flags after the ping-pong buffer
+    int* flags = passes > 1 ? reinterpret_cast<int*>(reinterpret_cast<char*>(ws) + adf_flags_offset(W, H, B))
+                            : nullptr;
+    if (flags) {
+        cudaError_t e = cudaMemsetAsync(flags, 0, sizeof(int) * (size_t)B, stream);
+        if (e != cudaSuccess) return e;
+    }
     const float* src = in;
     int done = 0;
     for (int k = 0; k < passes; ++k) {
@@ -384,7 +459,7 @@ cudaError_t adf_run(const float* in, float* out, float* normals, float* ws, int 
         float* dst = (((passes - 1 - k) & 1) == 0) ? out : ws;   // the last pass lands in `out`
         const bool last = k == passes - 1;
         cudaError_t e = launch_pass(src, dst, last ? normals : nullptr, W, H, B, it, last && normals != nullptr,
-                                    p, stream);
+                                    p, stream, flags, flags ? (k == 0 ? 1 : 2) : 0);
         if (e != cudaSuccess) return e;
         src = dst;
         done += it;

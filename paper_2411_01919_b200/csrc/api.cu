@@ -105,7 +105,7 @@ extern "C" {
 
 PM_API size_t pm_adf_workspace_bytes(int32_t W, int32_t H, int32_t n_frames) {
     if (W < 1 || H < 1 || n_frames < 1) return 0;
-    return (sizeof(float) * (size_t)n_frames * W * H + 255) & ~(size_t)255;
+    return pm::adf_flags_offset(W, H, n_frames) + ((sizeof(int) * (size_t)n_frames + 255) & ~(size_t)255);
 }
 
 PM_API pm_status pm_adf_filter(const float* depth_in, float* depth_out, int32_t W, int32_t H,

@@ -11,6 +11,8 @@ namespace pm {
 // ---- adf.cu
 cudaError_t adf_setup_attributes();
 int adf_default_iters_per_pass();
+// byte offset of the per-frame validity flags inside the adf workspace
+size_t adf_flags_offset(int W, int H, int B);
 // in -> out (B frames); ws: B*H*W floats (used when >= 2 passes); normals nullable.
 cudaError_t adf_run(const float* in, float* out, float* normals, float* ws, int W, int H, int B,
                     const pm_intrinsics* K, float lam, float kappa, int iters, int iters_per_pass,
