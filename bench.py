@@ -39,6 +39,23 @@ LAM, KAPPA, TAU, SEED = 0.15, 0.03, 0.01, 0x1919
 # algorithmic bytes of the fused ADF+normals stage per pixel: read depth 4 B,
 # write filtered depth 4 B, write normals 12 B
 ADF_ALG_BYTES_PX = 20
+# FP32 lane-ops of one Alg. 1 sweep at one pixel: 2gx, 2gy,
+# gy^2, gx^2+, exponent FFMA, ex2, three adds and an FFMA for the Laplacian,
+# the update FFMA
+ADF_OPS_PER_PIX_ITER = 11
+# one RANSAC point-hypothesis evaluation: 3 FFMA (n.p + d), compare, count
+RANSAC_OPS_PER_EVAL = 5
+
+
+def _ncu_traffic():
+    """DRAM bytes (read + write) of one ADF+normals stage on this workload,
+    from the committed ncu capture profiles/adf_traffic.json (same unit as
+    `achieved`: the whole stage), or None."""
+    p = os.path.join(ROOT, "profiles", "adf_traffic.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f).get("bytes_per_stage")
+    return None
 
 
 def _peaks():
@@ -57,7 +74,7 @@ class ClockSampler:
                0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
                0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
 
-    def __init__(self, index: int, period_s: float = 0.005):
+    def __init__(self, index: int, period_s: float = 0.002):
         self.index, self.period = index, period_s
         self.samples, self.reasons = [], set()
         self._stop = threading.Event()
@@ -101,6 +118,26 @@ class ClockSampler:
             return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"]}
         return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
                 "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# --------------------------------------------------------------------------- sharding
+def shard(rank: int, frames_per_rank: int):
+    """Frames of the C4 stream owned by `rank`: [rank * B, (rank + 1) * B).
+    The RNG is keyed by the global frame id, so every sharding gives the
+    same per-frame results (weak scaling, no data-path collective)."""
+    return rank * frames_per_rank, frames_per_rank
+
+
+def gather_tables(t, world: int, rank: int):
+    """Gather every rank's plane table to rank 0 (the only collective of the
+    path); returns the concatenation on rank 0, else None."""
+    import torch
+    import torch.distributed as dist
+    if world == 1:
+        return t
+    parts = [torch.empty_like(t) for _ in range(world)] if rank == 0 else None
+    dist.gather(t, parts, dst=0)
+    return torch.cat(parts) if rank == 0 else None
 
 
 # --------------------------------------------------------------------------- oracle arm
@@ -175,8 +212,7 @@ def run_cuda(args, rank, world, local_rank):
 
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
-    B = args.frames_per_rank
-    first = rank * B
+    first, B = shard(rank, args.frames_per_rank)
     # inputs: distinct frames of the C4 stream, generated on the device and kept resident in HBM
     depth, labels, K = scenegen.stair_stream(first, B, W, H, REGIONS, device=dev)
     depth_out = torch.empty_like(depth)
@@ -199,12 +235,15 @@ def run_cuda(args, rank, world, local_rank):
     barrier()
     torch.cuda.synchronize(dev)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    old_switch = sys.getswitchinterval()
+    sys.setswitchinterval(2e-4)          # let the NVML sampler thread run between launches
     with ClockSampler(dev.index if dev.index is not None else 0) as clocks:
         ev0.record(stream)
         for _ in range(args.steps):
             step()
         ev1.record(stream)
         torch.cuda.synchronize(dev)
+    sys.setswitchinterval(old_switch)
     barrier()
     torch.cuda.synchronize(dev)
     ms = ev0.elapsed_time(ev1)
@@ -231,11 +270,16 @@ def run_cuda(args, rank, world, local_rank):
     rs_t = statistics.median(rs_ms) / 1e3
     peak, peak_src = _peaks()
     adf_bytes = ADF_ALG_BYTES_PX * W * H * B
-    achieved = adf_bytes / adf_t / 1e9
+    achieved_hbm = adf_bytes / adf_t / 1e9
     n_pass = pm.pipeline_kernel_launches(ITERS, 0)
-    # FP32/MUFU view of the same stage: pixel-iterations per second
+    # ALU view of the same stage: Alg. 1 ℓ4-6 costs ADF_OPS_PER_PIX_ITER
+    # FP32 lane-operations per pixel-iteration; the stage's binding roofline is
+    # the SM issue/FP32 rate 148 SMs x 128 lanes x the SM clock.
     pix_iter_per_s = ITERS * W * H * B / adf_t
-
+    alu_peak = 148 * 128 * (clocks.max_mhz or 1965) * 1e6 / 1e12          # T lane-ops/s
+    alu_achieved = pix_iter_per_s * ADF_OPS_PER_PIX_ITER / 1e12
+    rs_evals_per_s = HYPS * W * H * B / rs_t
+    traffic = _ncu_traffic()
     # ---- e2e: host-resident inputs through the public API, H2D + compute + D2H of the plane table
     h_depth = depth.cpu().pin_memory()
     h_labels = labels.cpu().pin_memory()
@@ -265,12 +309,7 @@ def run_cuda(args, rank, world, local_rank):
     e2e_value = world * B * args.steps / (float(te.item()) / 1e3)
 
     # ---- final gather of the plane tables (the only collective)
-    if world > 1:
-        gathered = [torch.empty_like(planes) for _ in range(world)] if rank == 0 else None
-        if rank == 0:
-            dist.gather(planes, gathered, dst=0)
-        else:
-            dist.gather(planes, None, dst=0)
+    gather_tables(planes, world, rank)
 
     # ---- oracle baseline on the host cores (rank 0, N = 1 only)
     cpu = None
@@ -300,12 +339,21 @@ def run_cuda(args, rank, world, local_rank):
                        "frames_per_rank": B, "global_frames_per_step": world * B,
                        "l2": f"inputs larger than L2 ({B * W * H * 8 / 2**20:.0f} MiB depth+labels per rank)",
                        "parallelism": f"frame-sharded x{world}"},
-            "roofline": {"bound": "hbm", "kernel": f"adf_filter stage ({n_pass} pass launches, last fused with "
-                                                   "normals)",
-                         "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": None, "peak_source": peak_src,
-                         "alg_bytes_per_launch": adf_bytes, "stage_ms": adf_t * 1e3,
-                         "pixel_iters_per_s": pix_iter_per_s},
+            "roofline": {"bound": "alu", "kernel": f"adf_pass_kernel (ADF+normals stage: {n_pass} launches, "
+                                                   "last fused with the normals)",
+                         "achieved": alu_achieved, "peak": alu_peak, "unit": "T FP32 lane-op/s",
+                         "frac": alu_achieved / alu_peak, "traffic": traffic,
+                         "peak_source": "148 SMs x 128 FP32 lanes x max SM clock (B200_PROFILING.md)",
+                         "alg_ops_per_pixel_iter": ADF_OPS_PER_PIX_ITER, "pixel_iters_per_s": pix_iter_per_s,
+                         "hbm": {"achieved": achieved_hbm, "peak": peak, "unit": "GB/s",
+                                 "frac": achieved_hbm / peak, "alg_bytes_per_stage": adf_bytes,
+                                 "peak_source": peak_src}},
+            "ransac_roofline": {"bound": "alu", "kernel": "ransac_score_kernel (Alg. 2 l.9-13)",
+                                "achieved": rs_evals_per_s * RANSAC_OPS_PER_EVAL / 1e12, "peak": alu_peak,
+                                "unit": "T FP32 lane-op/s",
+                                "frac": rs_evals_per_s * RANSAC_OPS_PER_EVAL / 1e12 / alu_peak,
+                                "evals_per_s": rs_evals_per_s, "alg_ops_per_eval": RANSAC_OPS_PER_EVAL,
+                                "stage_ms_incl_compaction_refit": rs_t * 1e3},
             "stages_ms": {"adf_normals": adf_t * 1e3, "ransac_incl_compaction": rs_t * 1e3},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "frames/s", "h2d_bytes_per_step": B * W * H * 8,
