@@ -34,7 +34,7 @@ namespace pm {
 
 namespace {
 
-constexpr int kThreads = 256;      // 8 warps
+constexpr int kThreads = 256;      // 8 warps (3 CTAs / SM: shared memory bound)
 constexpr int kWarps = kThreads / 32;
 constexpr int kMaxItersPerPass = 16;
 
@@ -87,9 +87,10 @@ template <int SH, int PAD, bool CHECK>
 PM_DEVINL void sweep(const float* __restrict__ cur, float* __restrict__ nxt, int t, const Box& b,
                      float kc, float l2lam) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    constexpr int kParts = kWarps / 4;
     const int x = (warp & 3) * 32 + lane;
     const int ylo = max(t, b.iy0), yhi = min(SH - t, b.iy1);
-    const int half = (yhi - ylo + 1) >> 1;
+    const int half = (yhi - ylo + kParts - 1) / kParts;
     const int ys = ylo + (warp >> 2) * half;
     const int ye = min(ys + half, yhi);
     if (x < max(PAD + t, b.ix0) || x >= min(kSW - PAD - t, b.ix1) || ys >= ye) return;
@@ -129,9 +130,10 @@ template <int SH, int PAD, bool CHECK>
 PM_DEVINL void sweep_pairs(const float* __restrict__ cur, float* __restrict__ nxt, int t, const Box& b,
                            float kc, float l2lam) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    constexpr int kParts = kWarps / 2;
     const int x = ((warp & 1) * 32 + lane) * 2;
     const int ylo = max(t, b.iy0), yhi = min(SH - t, b.iy1);
-    const int q = (yhi - ylo + 3) >> 2;
+    const int q = (yhi - ylo + kParts - 1) / kParts;
     const int ys = ylo + (warp >> 1) * q;
     const int ye = min(ys + q, yhi);
     const int xa = max(PAD + t, b.ix0), xb = min(kSW - PAD - t, b.ix1);

@@ -26,6 +26,7 @@ namespace {
 
 constexpr unsigned kFull = 0xFFFFFFFFu;
 constexpr int kWarpsPerBlock = 8;
+constexpr int kPrefetch = 4;          // 32-pixel steps whose loads are issued together
 
 PM_DEVINL unsigned lanemask_lt() {
     unsigned m;
@@ -55,25 +56,37 @@ compact_count_kernel(const float* __restrict__ depth, const int32_t* __restrict_
     const size_t beg = (size_t)st * sub_tile;
     const size_t end = min(beg + (size_t)sub_tile, (size_t)WH);
     int cur = -1, cnt = 0;
-    for (size_t i0 = beg; i0 < end; i0 += 32) {
-        const int lab = pixel_label(d, l, i0 + lane, end, R);
-        if (__all_sync(kFull, lab == cur || lab < 0)) {
-            cnt += __popc(__ballot_sync(kFull, lab >= 0));
-            continue;
+    for (size_t i00 = beg; i00 < end; i00 += 32 * kPrefetch) {
+        int lraw[kPrefetch];
+        float zraw[kPrefetch];
+#pragma unroll
+        for (int u = 0; u < kPrefetch; ++u) {        // all loads of kPrefetch steps in flight
+            const size_t i = i00 + u * 32 + lane;
+            lraw[u] = i < end ? __ldg(l + i) : -1;
+            zraw[u] = i < end ? __ldg(d + i) : 0.0f;
         }
-        const int L = __reduce_max_sync(kFull, lab);
-        if (cur >= 0 && lane == 0) h[(size_t)cur * n_sub + st] += cnt;
-        __syncwarp();
-        if (__all_sync(kFull, lab == L || lab < 0)) {          // one new label
-            cur = L;
-            cnt = __popc(__ballot_sync(kFull, lab >= 0));
-            continue;
+#pragma unroll
+        for (int u = 0; u < kPrefetch; ++u) {
+            if (i00 + u * 32 >= end) break;
+            const int lab = (valid_depth(zraw[u]) && (unsigned)lraw[u] < (unsigned)R) ? lraw[u] : -1;
+            if (__all_sync(kFull, lab == cur || lab < 0)) {
+                cnt += __popc(__ballot_sync(kFull, lab >= 0));
+                continue;
+            }
+            const int L = __reduce_max_sync(kFull, lab);
+            if (cur >= 0 && lane == 0) h[(size_t)cur * n_sub + st] += cnt;
+            __syncwarp();
+            if (__all_sync(kFull, lab == L || lab < 0)) {          // one new label
+                cur = L;
+                cnt = __popc(__ballot_sync(kFull, lab >= 0));
+                continue;
+            }
+            cur = -1;                                              // mixed step
+            cnt = 0;
+            const unsigned m = __match_any_sync(kFull, lab);
+            if (lab >= 0 && lane == __ffs(m) - 1) h[(size_t)lab * n_sub + st] += __popc(m);
+            __syncwarp();
         }
-        cur = -1;                                              // mixed step
-        cnt = 0;
-        const unsigned m = __match_any_sync(kFull, lab);
-        if (lab >= 0 && lane == __ffs(m) - 1) h[(size_t)lab * n_sub + st] += __popc(m);
-        __syncwarp();
     }
     if (cur >= 0 && lane == 0) h[(size_t)cur * n_sub + st] += cnt;
 }
@@ -161,43 +174,56 @@ compact_scatter_kernel(const float* __restrict__ depth, const int32_t* __restric
     const size_t end = min(beg + (size_t)sub_tile, (size_t)WH);
     const unsigned lt = lanemask_lt();
     int cur = -1, rel = 0, roff = 0;       // cached label, next rank within region, region offset
-    for (size_t i0 = beg; i0 < end; i0 += 32) {
-        const size_t i = i0 + lane;
-        const int lab = pixel_label(d, l, i, end, R);
-        uint2 pk = make_uint2(0u, 0u);
-        if (lab >= 0) {
-            const unsigned u = (unsigned)(i % (unsigned)W), v = (unsigned)(i / (unsigned)W);
-            pk = make_uint2(u | (v << 16), __float_as_uint(__ldg(d + i)));
+    for (size_t i00 = beg; i00 < end; i00 += 32 * kPrefetch) {
+        int lraw[kPrefetch];
+        float zraw[kPrefetch];
+#pragma unroll
+        for (int u = 0; u < kPrefetch; ++u) {        // all loads of kPrefetch steps in flight
+            const size_t i = i00 + u * 32 + lane;
+            lraw[u] = i < end ? __ldg(l + i) : -1;
+            zraw[u] = i < end ? __ldg(d + i) : 0.0f;
         }
-        bool fast = __all_sync(kFull, lab == cur || lab < 0);
-        if (!fast) {
-            const int L = __reduce_max_sync(kFull, lab);
-            if (cur >= 0 && lane == 0) h[(size_t)cur * n_sub + st] = rel;     // flush
-            __syncwarp();
-            if (__all_sync(kFull, lab == L || lab < 0)) {
-                cur = L;
-                rel = h[(size_t)L * n_sub + st];
-                roff = off[L];
-                fast = true;
-            } else {
-                cur = -1;
-                const unsigned m = __match_any_sync(kFull, lab);
-                const int leader = __ffs(m) - 1;
-                int b = 0;
-                if (lab >= 0 && lane == leader) {
-                    const int r0 = h[(size_t)lab * n_sub + st];
-                    h[(size_t)lab * n_sub + st] = r0 + __popc(m);
-                    b = off[lab] + r0;
-                }
-                b = __shfl_sync(kFull, b, leader);
-                if (lab >= 0) pts[b + __popc(m & lt)] = pk;
-                __syncwarp();
+#pragma unroll
+        for (int u = 0; u < kPrefetch; ++u) {
+            const size_t i0 = i00 + u * 32;
+            if (i0 >= end) break;
+            const size_t i = i0 + lane;
+            const int lab = (valid_depth(zraw[u]) && (unsigned)lraw[u] < (unsigned)R) ? lraw[u] : -1;
+            uint2 pk = make_uint2(0u, 0u);
+            if (lab >= 0) {
+                const unsigned uu = (unsigned)(i % (unsigned)W), vv = (unsigned)(i / (unsigned)W);
+                pk = make_uint2(uu | (vv << 16), __float_as_uint(zraw[u]));
             }
-        }
-        if (fast) {
-            const unsigned bal = __ballot_sync(kFull, lab >= 0);
-            if (lab >= 0) pts[roff + rel + __popc(bal & lt)] = pk;
-            rel += __popc(bal);
+            bool fast = __all_sync(kFull, lab == cur || lab < 0);
+            if (!fast) {
+                const int L = __reduce_max_sync(kFull, lab);
+                if (cur >= 0 && lane == 0) h[(size_t)cur * n_sub + st] = rel;     // flush
+                __syncwarp();
+                if (__all_sync(kFull, lab == L || lab < 0)) {
+                    cur = L;
+                    rel = h[(size_t)L * n_sub + st];
+                    roff = off[L];
+                    fast = true;
+                } else {
+                    cur = -1;
+                    const unsigned m = __match_any_sync(kFull, lab);
+                    const int leader = __ffs(m) - 1;
+                    int b = 0;
+                    if (lab >= 0 && lane == leader) {
+                        const int r0 = h[(size_t)lab * n_sub + st];
+                        h[(size_t)lab * n_sub + st] = r0 + __popc(m);
+                        b = off[lab] + r0;
+                    }
+                    b = __shfl_sync(kFull, b, leader);
+                    if (lab >= 0) pts[b + __popc(m & lt)] = pk;
+                    __syncwarp();
+                }
+            }
+            if (fast) {
+                const unsigned bal = __ballot_sync(kFull, lab >= 0);
+                if (lab >= 0) pts[roff + rel + __popc(bal & lt)] = pk;
+                rel += __popc(bal);
+            }
         }
     }
     if (cur >= 0 && lane == 0) h[(size_t)cur * n_sub + st] = rel;

@@ -333,17 +333,26 @@ ransac_refit_kernel(RansacWorkspace ws, RansacArgs a) {
             const float3 o3 = deproject(PackedPoint{q0.x, __uint_as_float(q0.y)}, a.K.cx, a.K.cy, ifx, ify);
             const double ox = o3.x, oy = o3.y, oz = o3.z;
             Sums acc = {};
-            for (int i = lo + threadIdx.x; i < hi; i += kScoreThreads) {
-                const uint2 q = pts[i];
-                const float3 P = deproject(PackedPoint{q.x, __uint_as_float(q.y)}, a.K.cx, a.K.cy, ifx, ify);
-                const float dist = plane_dist(pl, P);
-                acc.err += __float2ull_rn(__fmul_rn(fminf(dist, 64.0f), 16777216.0f));
-                if (dist < a.tau) {
-                    const double x = (double)P.x - ox, y = (double)P.y - oy, z = (double)P.z - oz;
-                    acc.s[0] += x; acc.s[1] += y; acc.s[2] += z;
-                    acc.m[0] = fma(x, x, acc.m[0]); acc.m[1] = fma(x, y, acc.m[1]); acc.m[2] = fma(x, z, acc.m[2]);
-                    acc.m[3] = fma(y, y, acc.m[3]); acc.m[4] = fma(y, z, acc.m[4]); acc.m[5] = fma(z, z, acc.m[5]);
-                    acc.n += 1;
+            for (int i0 = lo + threadIdx.x; i0 < hi; i0 += 4 * kScoreThreads) {
+                uint2 qs[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {                 // 4 loads in flight per thread
+                    const int i = i0 + u * kScoreThreads;
+                    qs[u] = i < hi ? pts[i] : make_uint2(0u, 0u);
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    if (i0 + u * kScoreThreads >= hi) break;
+                    const float3 P = deproject(PackedPoint{qs[u].x, __uint_as_float(qs[u].y)}, a.K.cx, a.K.cy, ifx, ify);
+                    const float dist = plane_dist(pl, P);
+                    acc.err += __float2ull_rn(__fmul_rn(fminf(dist, 64.0f), 16777216.0f));
+                    if (dist < a.tau) {
+                        const double x = (double)P.x - ox, y = (double)P.y - oy, z = (double)P.z - oz;
+                        acc.s[0] += x; acc.s[1] += y; acc.s[2] += z;
+                        acc.m[0] = fma(x, x, acc.m[0]); acc.m[1] = fma(x, y, acc.m[1]); acc.m[2] = fma(x, z, acc.m[2]);
+                        acc.m[3] = fma(y, y, acc.m[3]); acc.m[4] = fma(y, z, acc.m[4]); acc.m[5] = fma(z, z, acc.m[5]);
+                        acc.n += 1;
+                    }
                 }
             }
 #pragma unroll
