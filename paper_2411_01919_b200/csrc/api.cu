@@ -18,7 +18,10 @@ std::once_flag g_once;
 cudaError_t g_setup_err = cudaSuccess;
 
 cudaError_t setup() {
-    std::call_once(g_once, [] { g_setup_err = pm::adf_setup_attributes(); });
+    std::call_once(g_once, [] {
+        g_setup_err = pm::adf_setup_attributes();
+        if (g_setup_err == cudaSuccess) g_setup_err = pm::ransac_setup_attributes();
+    });
     return g_setup_err;
 }
 

@@ -34,15 +34,6 @@ PM_DEVINL unsigned lanemask_lt() {
     return m;
 }
 
-// Label of pixel i for region purposes: -1 unless 0 <= label < R and depth valid.
-PM_DEVINL int pixel_label(const float* __restrict__ depth, const int32_t* __restrict__ labels,
-                          size_t i, size_t end, int R) {
-    if (i >= end) return -1;
-    const int l = __ldg(labels + i);
-    const float z = __ldg(depth + i);
-    return (valid_depth(z) && (unsigned)l < (unsigned)R) ? l : -1;
-}
-
 __global__ void __launch_bounds__(kWarpsPerBlock * 32)
 compact_count_kernel(const float* __restrict__ depth, const int32_t* __restrict__ labels,
                      int WH, int R, int sub_tile, int n_sub, int32_t* __restrict__ hist) {

@@ -52,6 +52,7 @@ struct RansacArgs {
     int32_t* counts_out;   // nullable debug
     uint64_t* errq_out;    // nullable debug
 };
+cudaError_t ransac_setup_attributes();
 cudaError_t ransac_run(const RansacWorkspace& ws, const RansacArgs& a, pm_plane* planes,
                        cudaStream_t stream);
 

@@ -17,7 +17,6 @@
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
-#include <stdlib.h>
 
 #include "common.cuh"
 #include "internal.h"
@@ -37,7 +36,7 @@ namespace {
 
 constexpr unsigned kFull = 0xFFFFFFFFu;
 constexpr int kScoreThreads = 256;
-constexpr int kChunk = 2048;          // points per scoring CTA
+constexpr int kScoreChunk = 4096;     // points per scoring CTA (dynamic shared memory)
 constexpr int kHB = 8;                // hypothesis array padding
 constexpr int kRefitChunk = 8192;     // points per refit CTA
 
@@ -133,12 +132,13 @@ struct Chunk {
 
 PM_DEVINL bool stage_chunk(const RansacWorkspace& ws, const RansacArgs& a, size_t f, float4* sp, int* s_r0,
                            Chunk& ck) {
+    // points per CTA: kScoreChunk
     const int R = ws.R;
     const int32_t* off = ws.region_off + f * (size_t)(R + 1);
     const int total = off[R];
-    ck.s = blockIdx.x * kChunk;
+    ck.s = blockIdx.x * kScoreChunk;
     if (ck.s >= total) return false;
-    ck.e = min(ck.s + kChunk, total);
+    ck.e = min(ck.s + kScoreChunk, total);
     const uint2* pts = ws.points + f * (size_t)ws.W * ws.H;
     const float ifx = 1.0f / a.K.fx, ify = 1.0f / a.K.fy;   // IEEE division, as on the host
     for (int i = threadIdx.x; i < ck.e - ck.s; i += kScoreThreads) {
@@ -164,26 +164,26 @@ PM_DEVINL void count_lt(int& c, float a, float b) {
     asm("{\n.reg .pred p;\nsetp.lt.f32 p, %1, %2;\n@p add.s32 %0, %0, 1;\n}" : "+r"(c) : "f"(a), "f"(b));
 }
 
-// The hot loop (Alg. 2 ℓ9-13).  grid = (ceil(W*H / kChunk), B).  The CTA's
+// The hot loop (Alg. 2 ℓ9-13).  grid = (ceil(W*H / kScoreChunk), B).  The CTA's
 // threads form G = 256 / L groups of L lanes; lane l of every group holds
 // hypotheses l, l + L, ..., l + (K-1) L of the current region in registers;
 // group g walks points g, g + G, ... of the segment, each point a broadcast
 // shared load.  An evaluation costs 3 FFMA + FSETP + a predicated IADD; the
 // only reduction is one shared-memory sum over the G groups per segment and
 // one integer atomic per hypothesis (exact and order-free).
-template <int K, bool WITH_ERR>
+template <int K, int L, bool WITH_ERR>
 __global__ void __launch_bounds__(kScoreThreads)
-ransac_score_kernel(RansacWorkspace ws, RansacArgs a, int L) {
-    __shared__ float4 sp[kChunk];
+ransac_score_kernel(RansacWorkspace ws, RansacArgs a) {
+    extern __shared__ __align__(16) float4 sp[];                 // kScoreChunk points
     __shared__ int s_r0;
-    constexpr bool kSmemReduce = K <= 8;     // K = 16 would exceed the 48 KB static limit
-    __shared__ int s_cnt[kScoreThreads * (kSmemReduce ? K : 1)];
+    constexpr int G = kScoreThreads / L;
+    constexpr bool kSmemReduce = G > 1;
+    int* s_cnt = reinterpret_cast<int*>(sp + kScoreChunk);      // [G][L * K]
     const size_t f = blockIdx.y;
     Chunk ck;
     if (!stage_chunk(ws, a, f, sp, &s_r0, ck)) return;
     const int R = ws.R, HP = ws.n_hyp_pad, NH = ws.n_hyp;
-    const int G = kScoreThreads / L;
-    const int g = threadIdx.x / L, l = threadIdx.x - g * L;
+    const int g = threadIdx.x / L, l = threadIdx.x % L;
     const int32_t* off = ws.region_off + f * (size_t)(R + 1);
     const float tau = a.tau;
     const float4 nan4 = make_float4(__int_as_float(0x7FC00000), 0.f, 0.f, 0.f);
@@ -222,7 +222,7 @@ ransac_score_kernel(RansacWorkspace ws, RansacArgs a, int L) {
                     atomicAdd((unsigned long long*)(errq + h), (unsigned long long)eq[k]);
             }
         }
-        if (G == 1 || !kSmemReduce) {
+        if (!kSmemReduce) {
 #pragma unroll
             for (int k = 0; k < K; ++k) {
                 const int h = l + k * L;
@@ -488,6 +488,20 @@ ransac_finalize_kernel(RansacWorkspace ws, RansacArgs a, pm_plane* __restrict__ 
 
 static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
+cudaError_t ransac_setup_attributes() {
+    cudaError_t e = cudaSuccess;
+#define PM_ATTR(KK, LL)                                                                                    \
+    for (int wr = 0; wr < 2 && e == cudaSuccess; ++wr)                                                     \
+        e = cudaFuncSetAttribute(wr ? (const void*)ransac_score_kernel<KK, LL, true>                        \
+                                    : (const void*)ransac_score_kernel<KK, LL, false>,                      \
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize,                              \
+                                 (int)(sizeof(float4) * kScoreChunk + sizeof(int) * kScoreThreads * KK));
+    PM_ATTR(1, 8) PM_ATTR(2, 8) PM_ATTR(4, 8) PM_ATTR(8, 8) PM_ATTR(8, 16) PM_ATTR(8, 32)
+    PM_ATTR(8, 64) PM_ATTR(8, 128) PM_ATTR(8, 256) PM_ATTR(16, 256)
+#undef PM_ATTR
+    return e;
+}
+
 RansacWorkspace ransac_workspace_layout(void* base, int W, int H, int R, int n_hyp, int B) {
     RansacWorkspace ws{};
     ws.W = W; ws.H = H; ws.B = B; ws.R = R; ws.n_hyp = n_hyp;
@@ -519,22 +533,25 @@ cudaError_t ransac_run(const RansacWorkspace& ws, const RansacArgs& a, pm_plane*
     const bool need_err = a.select == PM_SELECT_ERROR || a.errq_out != nullptr;
     const int n_hyp_slots = ws.R * ws.n_hyp_pad;
     ransac_hyp_kernel<<<dim3((n_hyp_slots + 255) / 256, ws.B), 256, 0, stream>>>(ws, a, need_err ? 1 : 0);
-    const dim3 g_chunks((unsigned)(((size_t)ws.W * ws.H + kChunk - 1) / kChunk), ws.B);
     // K hypotheses per lane, L lanes per group (L * K >= n_hyp): small L
     // means more points in flight per warp and a cheaper per-point overhead
     auto pow2ceil = [](int x) { int p = 1; while (p < x) p <<= 1; return p; };
     int L = pow2ceil((ws.n_hyp + 7) / 8);
     L = L < 8 ? 8 : (L > 256 ? 256 : L);
-    if (const char* e = getenv("PM_SCORE_LANES")) { const int v = atoi(e); if (v >= 8 && v <= 256 && (v & (v - 1)) == 0) L = v; }
-    int K = pow2ceil((ws.n_hyp + L - 1) / L);
-    if (K > 16) { K = 16; L = pow2ceil((ws.n_hyp + 15) / 16); }
-#define PM_SCORE(KK)                                                                              \
-    if (K == KK) {                                                                                \
-        if (need_err) ransac_score_kernel<KK, true><<<g_chunks, kScoreThreads, 0, stream>>>(ws, a, L);  \
-        else ransac_score_kernel<KK, false><<<g_chunks, kScoreThreads, 0, stream>>>(ws, a, L);         \
+    const int K = pow2ceil((ws.n_hyp + L - 1) / L);     // <= 8 except n_hyp > 2048 -> 16
+    const dim3 g_score((unsigned)(((size_t)ws.W * ws.H + kScoreChunk - 1) / kScoreChunk), ws.B);
+    const size_t smem = sizeof(float4) * kScoreChunk + sizeof(int) * kScoreThreads * K;
+    bool launched = false;
+#define PM_SCORE(KK, LL)                                                                                   \
+    if (K == KK && L == LL) {                                                                              \
+        if (need_err) ransac_score_kernel<KK, LL, true><<<g_score, kScoreThreads, smem, stream>>>(ws, a);  \
+        else ransac_score_kernel<KK, LL, false><<<g_score, kScoreThreads, smem, stream>>>(ws, a);          \
+        launched = true;                                                                                   \
     }
-    PM_SCORE(1) PM_SCORE(2) PM_SCORE(4) PM_SCORE(8) PM_SCORE(16)
+    PM_SCORE(1, 8) PM_SCORE(2, 8) PM_SCORE(4, 8) PM_SCORE(8, 8) PM_SCORE(8, 16) PM_SCORE(8, 32)
+    PM_SCORE(8, 64) PM_SCORE(8, 128) PM_SCORE(8, 256) PM_SCORE(16, 256)
 #undef PM_SCORE
+    if (!launched) return cudaErrorInvalidConfiguration;
     const dim3 g_refit((unsigned)(((size_t)ws.W * ws.H + kRefitChunk - 1) / kRefitChunk), ws.B);
     ransac_refit_kernel<<<g_refit, kScoreThreads, 0, stream>>>(ws, a);
     ransac_finalize_kernel<<<dim3((ws.R + kFinalThreads - 1) / kFinalThreads, ws.B), kFinalThreads, 0, stream>>>(
