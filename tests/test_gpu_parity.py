@@ -214,3 +214,75 @@ def test_pipeline_end_to_end(pm):
     assert np.array_equal(planes.best_hyp.cpu().numpy(), ref["best_hyp"])
     assert np.array_equal(planes.status.cpu().numpy(), ref["status"])
     assert (ref["status"] == 0).mean() > 0.9
+
+
+# --------------------------------------------------------------------------
+# BASELINE.json full-size configurations, in the launch configuration the
+# bench uses, checked on samples the oracle can compute.
+def _crop_adf_check(pm, d_in, d_gpu, lam, kappa, iters, rng, n=6, size=48):
+    """ADF is local: after N sweeps a pixel depends only on pixels within N
+    (L1) of it, so the oracle on a crop with an N-pixel margin reproduces the
+    crop's centre exactly (the crop border acts as a zero-flux edge only for
+    pixels that are discarded)."""
+    H, W = d_in.shape
+    m = iters
+    for _ in range(n):
+        y = int(rng.integers(0, max(1, H - size)))
+        x = int(rng.integers(0, max(1, W - size)))
+        y0, x0 = max(0, y - m), max(0, x - m)
+        y1, x1 = min(H, y + size + m), min(W, x + size + m)
+        ref = oracle.adf(np.ascontiguousarray(d_in[y0:y1, x0:x1]), lam, kappa, iters)
+        cy0, cx0 = y - y0, x - x0
+        sub_ref = ref[cy0:cy0 + size, cx0:cx0 + size]
+        sub_in = d_in[y:y + size, x:x + size]
+        _check_depth(d_gpu[y:y + size, x:x + size], sub_in, sub_ref)
+
+
+@pytest.mark.parametrize("name", ["C3", "C5"])
+def test_full_size_configs_sampled(pm, name):
+    fr = scenegen.make_config(name)
+    rng = np.random.default_rng(42)
+    d_in = fr["depth"].numpy()
+    dev_d = fr["depth"].to(DEV)
+    d_out, nrm = pm.adf_filter(dev_d, fr["K"], fr["lam"], fr["kappa"], fr["iters"])
+    torch.cuda.synchronize()
+    d_gpu = d_out.cpu().numpy()
+    _crop_adf_check(pm, d_in, d_gpu, fr["lam"], fr["kappa"], fr["iters"], rng)
+    # normals: oracle on crops of the GPU depth (+1 margin), compared on the centre
+    n_gpu = nrm.cpu().numpy()
+    H, W = d_gpu.shape
+    for _ in range(6):
+        y, x = int(rng.integers(0, H - 64)), int(rng.integers(0, W - 64))
+        y0, x0, y1, x1 = max(0, y - 1), max(0, x - 1), min(H, y + 65), min(W, x + 65)
+        ref = oracle.normals(np.ascontiguousarray(d_gpu[y0:y1, x0:x1]), scenegen.Intrinsics(
+            fr["K"].fx, fr["K"].fy, fr["K"].cx - x0, fr["K"].cy - y0))
+        cy, cx = y - y0, x - x0
+        _check_normals(n_gpu[:, y:y + 64, x:x + 64], ref[:, cy:cy + 64, cx:cx + 64])
+    # RANSAC over every region of the full frame (GPU-filtered depth), bit-exact
+    _ransac_compare(pm, d_gpu, fr["labels"].numpy(), fr["K"], fr["n_regions"], fr["n_hyp"], fr["tau"], fr["seed"])
+
+
+def test_bench_configuration_sampled(pm):
+    """The bench's workload (C4 stream, 512 frames per call, pm_process_frames):
+    frames 0, 511 and one in between checked against the oracle."""
+    import bench
+    B = 512
+    first, _ = bench.shard(0, B)
+    d, lab, K = scenegen.stair_stream(first, B, bench.W, bench.H, bench.REGIONS, device=DEV)
+    d_out, nrm, planes = pm.process_frames(d, lab, K, bench.LAM, bench.KAPPA, bench.ITERS, bench.REGIONS,
+                                           bench.HYPS, bench.TAU, bench.SEED, first_frame_id=first)
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(7)
+    for i in [0, int(rng.integers(1, B - 1)), B - 1]:
+        d_in = d[i].cpu().numpy()
+        d_gpu = d_out[i].cpu().numpy()
+        _check_depth(d_gpu, d_in, oracle.adf(d_in, bench.LAM, bench.KAPPA, bench.ITERS))
+        _check_normals(nrm[i].cpu().numpy(), oracle.normals(d_gpu, K))
+        ref = oracle.ransac(d_gpu, lab[i].cpu().numpy(), K, bench.REGIONS, bench.HYPS, bench.TAU, bench.SEED,
+                            frame_id=first + i)
+        assert np.array_equal(planes.best_hyp[i].cpu().numpy(), ref["best_hyp"])
+        assert np.array_equal(planes.inliers[i].cpu().numpy(), ref["inliers"])
+        assert np.array_equal(planes.status[i].cpu().numpy(), ref["status"])
+        ok = ref["status"] <= 1
+        assert np.abs(planes.n[i].cpu().numpy()[ok] - ref["n"][ok]).max() <= REFIT_TOL
+        assert np.abs(planes.centroid[i].cpu().numpy()[ok] - ref["centroid"][ok]).max() <= REFIT_TOL
