@@ -108,9 +108,19 @@ PM_API pm_status pm_adf_filter_batched(const float* depth_in, float* depth_out, 
                                        void* workspace, size_t ws_bytes, pm_stream_t stream);
 PM_API size_t pm_adf_workspace_bytes(int32_t W, int32_t H, int32_t n_frames);
 
-/* Tuning / test knobs for adf (results do not depend on them). */
+/* Options for adf.  iters_per_pass is a tuning knob (results do not depend
+ * on it); scheme / normals_mode select the paper-literal variants (NEXT-1):
+ *   PM_ADF_ALG1        Alg. 1 as printed, c_p * lap(I) (default, Q1)
+ *   PM_ADF_DIVERGENCE  Eq. 1 as the 4-flux Perona-Malik scheme
+ *                      I += lambda * sum_d exp(-((I_d - I)/k)^2) (I_d - I)
+ *   PM_NORMALS_GEOMETRIC   the tangent-cross-product normal (default, Q7)
+ *   PM_NORMALS_AS_PRINTED  Eq. 2 literally: n = -K^-1 [Gx, Gy, 1]^T, normalised */
+enum { PM_ADF_ALG1 = 0, PM_ADF_DIVERGENCE = 1 };
+enum { PM_NORMALS_GEOMETRIC = 0, PM_NORMALS_AS_PRINTED = 1 };
 typedef struct {
-    int32_t iters_per_pass;   /* temporal blocking depth T per HBM pass; 0 = default */
+    int32_t iters_per_pass;   /* temporal blocking depth T per HBM pass (1..16); 0 = default */
+    int32_t scheme;           /* PM_ADF_*     */
+    int32_t normals_mode;     /* PM_NORMALS_* */
 } pm_adf_options;
 PM_API pm_status pm_adf_filter_ex(const float* depth_in, float* depth_out, int32_t W, int32_t H,
                                   int32_t n_frames, const pm_intrinsics* K, float lambda,
@@ -132,6 +142,10 @@ PM_API pm_status pm_normals_from_depth(const float* depth, int32_t W, int32_t H,
 PM_API pm_status pm_normals_from_depth_batched(const float* depth, int32_t W, int32_t H,
                                                int32_t n_frames, const pm_intrinsics* K,
                                                float* normals_out, pm_stream_t stream);
+/* mode: PM_NORMALS_GEOMETRIC (default) or PM_NORMALS_AS_PRINTED (see pm_adf_options). */
+PM_API pm_status pm_normals_from_depth_ex(const float* depth, int32_t W, int32_t H, int32_t n_frames,
+                                          const pm_intrinsics* K, int32_t mode, float* normals_out,
+                                          pm_stream_t stream);
 
 /* ---------------------------------------------------------------------- */
 /* ransac_planes — Algorithm 2, batched over every region of every

@@ -25,6 +25,8 @@ CFLAGS = ["-O2", "-std=c11", "-fPIC", "-shared", "-ffp-contract=off", "-fno-fast
           "-fvisibility=hidden", "-Wall", "-Wextra", "-Wno-unused-parameter"]
 
 SAMPLER_PHILOX, SAMPLER_ENUMERATE = 0, 1
+ADF_ALG1, ADF_DIVERGENCE = 0, 1
+NORMALS_GEOMETRIC, NORMALS_AS_PRINTED = 0, 1
 SELECT_COUNT, SELECT_ERROR = 0, 1
 STATUS_OK, STATUS_REJECTED, STATUS_TOO_FEW, STATUS_DEGENERATE = 0, 1, 2, 3
 
@@ -48,6 +50,9 @@ def lib() -> ctypes.CDLL:
             i32, u32, u64, f32, f64 = (ctypes.c_int, ctypes.c_uint32, ctypes.c_uint64,
                                        ctypes.c_float, ctypes.c_double)
             L.orc_adf.argtypes = [P, P, i32, i32, f64, f64, i32]
+            L.orc_adf_ex.argtypes = [P, P, i32, i32, f64, f64, i32, i32]
+            L.orc_normals_ex.argtypes = [P, i32, i32, f64, f64, f64, f64, i32, P]
+            L.orc_normals_f64_ex.argtypes = [P, i32, i32, f64, f64, f64, f64, i32, P]
             L.orc_normals.argtypes = [P, i32, i32, f64, f64, f64, f64, P]
             L.orc_normals_f64.argtypes = [P, i32, i32, f64, f64, f64, f64, P]
             L.orc_sobel_f64.argtypes = [P, i32, i32, P]
@@ -76,31 +81,33 @@ def _c(a, dtype) -> np.ndarray:
     return np.ascontiguousarray(a, dtype=dtype)
 
 
-def adf(depth: np.ndarray, lam: float, kappa: float, iters: int) -> np.ndarray:
-    """Alg. 1 ℓ1-8 on one f32 [H, W] frame (metres) -> f32 [H, W]."""
+def adf(depth: np.ndarray, lam: float, kappa: float, iters: int, scheme: int = ADF_ALG1) -> np.ndarray:
+    """Alg. 1 ℓ1-8 on one f32 [H, W] frame (metres) -> f32 [H, W].
+    scheme=ADF_DIVERGENCE: Eq. 1 as the 4-flux Perona-Malik scheme."""
     d = _c(depth, np.float32)
     H, W = d.shape
     out = np.empty_like(d)
-    rc = lib().orc_adf(_p(d), _p(out), W, H, float(lam), float(kappa), int(iters))
+    rc = lib().orc_adf_ex(_p(d), _p(out), W, H, float(lam), float(kappa), int(iters), int(scheme))
     assert rc == 0
     return out
 
 
-def normals(depth: np.ndarray, K) -> np.ndarray:
-    """Alg. 1 ℓ9-13 on f32 depth -> float64 [3, H, W]; (0,0,0) = invalid."""
+def normals(depth: np.ndarray, K, mode: int = NORMALS_GEOMETRIC) -> np.ndarray:
+    """Alg. 1 ℓ9-13 on f32 depth -> float64 [3, H, W]; (0,0,0) = invalid.
+    mode=NORMALS_AS_PRINTED: Eq. 2 literally."""
     d = _c(depth, np.float32)
     H, W = d.shape
     out = np.empty((3, H, W), np.float64)
-    rc = lib().orc_normals(_p(d), W, H, K.fx, K.fy, K.cx, K.cy, _p(out))
+    rc = lib().orc_normals_ex(_p(d), W, H, K.fx, K.fy, K.cx, K.cy, int(mode), _p(out))
     assert rc == 0
     return out
 
 
-def normals_f64(depth: np.ndarray, K) -> np.ndarray:
+def normals_f64(depth: np.ndarray, K, mode: int = NORMALS_GEOMETRIC) -> np.ndarray:
     d = _c(depth, np.float64)
     H, W = d.shape
     out = np.empty((3, H, W), np.float64)
-    rc = lib().orc_normals_f64(_p(d), W, H, K.fx, K.fy, K.cx, K.cy, _p(out))
+    rc = lib().orc_normals_f64_ex(_p(d), W, H, K.fx, K.fy, K.cx, K.cy, int(mode), _p(out))
     assert rc == 0
     return out
 

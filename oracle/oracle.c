@@ -36,6 +36,9 @@
 static int orc_valid_f(float z) { return z > 0.0f && isfinite(z); }
 static int orc_valid_d(double z) { return z > 0.0 && isfinite(z); }
 
+enum { ORC_ADF_ALG1 = 0, ORC_ADF_DIVERGENCE = 1 };
+enum { ORC_NORMALS_GEOMETRIC = 0, ORC_NORMALS_AS_PRINTED = 1 };
+
 /* ------------------------------------------------------------------------ */
 /* Algorithm 1, lines 1-8: anisotropic diffusion.
  *   ℓ1  I_smooth <- I
@@ -47,9 +50,11 @@ static int orc_valid_d(double z) { return z > 0.0 && isfinite(z); }
  * Boundary / invalid depth (Q4): an out-of-image or invalid neighbour takes
  * the centre pixel's value (zero flux); invalid pixels never change.
  * in/out: f32 [H][W] metres.  Computes in double, rounds once at the end.
+ * scheme ORC_ADF_DIVERGENCE: Eq. 1 as the 4-flux Perona-Malik scheme instead
+ * (NEXT-1; same zero-flux rule).
  * Returns 0, or -1 on bad arguments / allocation failure.                   */
-ORC_API int orc_adf(const float* in, float* out, int W, int H,
-                    double lambda, double kappa, int iters)
+ORC_API int orc_adf_ex(const float* in, float* out, int W, int H,
+                       double lambda, double kappa, int iters, int scheme)
 {
     if (!in || !out || W < 1 || H < 1 || iters < 0 || !(kappa > 0)) return -1;
     size_t n = (size_t)W * H;
@@ -72,11 +77,20 @@ ORC_API int orc_adf(const float* in, float* out, int W, int H,
                 double vs = (v < H - 1 && valid[p + W]) ? I[p + W] : c0;
                 double vw = (u > 0     && valid[p - 1]) ? I[p - 1] : c0;
                 double ve = (u < W - 1 && valid[p + 1]) ? I[p + 1] : c0;
-                double gx = 0.5 * (ve - vw);                 /* ℓ4 */
-                double gy = 0.5 * (vs - vn);
-                double c = exp(-(gx * gx + gy * gy) / k2);   /* ℓ5 */
-                double lap = (vn + vs + ve + vw) - 4.0 * c0;
-                J[p] = c0 + lambda * c * lap;                /* ℓ6 */
+                if (scheme == ORC_ADF_DIVERGENCE) {
+                    /* Eq. 1 discretised as the classic 4-flux
+                     * Perona-Malik scheme: I += lambda sum_d c(|grad_d I|) grad_d I,
+                     * grad_d I = I_d - I_p, c(x) = exp(-(x/k)^2) (Q1) */
+                    double dn = vn - c0, ds = vs - c0, dw = vw - c0, de = ve - c0;
+                    J[p] = c0 + lambda * (exp(-dn * dn / k2) * dn + exp(-ds * ds / k2) * ds +
+                                          exp(-dw * dw / k2) * dw + exp(-de * de / k2) * de);
+                } else {
+                    double gx = 0.5 * (ve - vw);             /* ℓ4 */
+                    double gy = 0.5 * (vs - vn);
+                    double c = exp(-(gx * gx + gy * gy) / k2);   /* ℓ5 */
+                    double lap = (vn + vs + ve + vw) - 4.0 * c0;
+                    J[p] = c0 + lambda * c * lap;            /* ℓ6 */
+                }
             }
         }
         double* t = I; I = J; J = t;                         /* Jacobi swap */
@@ -87,6 +101,12 @@ ORC_API int orc_adf(const float* in, float* out, int W, int H,
     return 0;
 }
 
+ORC_API int orc_adf(const float* in, float* out, int W, int H,
+                    double lambda, double kappa, int iters)
+{
+    return orc_adf_ex(in, out, W, H, lambda, kappa, iters, ORC_ADF_ALG1);
+}
+
 /* ------------------------------------------------------------------------ */
 /* Algorithm 1, lines 9-13 and Eq. 2: per-pixel
  * normal from Sobel gradients and the intrinsics K, read geometrically (Q7):
@@ -94,10 +114,12 @@ ORC_API int orc_adf(const float* in, float* out, int W, int H,
  *   m = dP/du x dP/dv for P(u,v) = Z(u,v) K^-1 [u v 1]^T, scaled by fx fy / Z:
  *   m = ( fx Gx, fy Gy, -(Z + (u-cx) Gx + (v-cy) Gy) ),  n = m / |m|  (ℓ12).
  * Invalid marker (Q9): n = (0,0,0) if any pixel of the clamped 3x3 window is
- * invalid.  depth: [H][W] double; out: [3][H][W] double (SoA).              */
-ORC_API int orc_normals_f64(const double* D, int W, int H,
-                            double fx, double fy, double cx, double cy,
-                            double* out)
+ * invalid.  mode ORC_NORMALS_AS_PRINTED: Eq. 2 literally, n = -K^-1[Gx,Gy,1]^T
+ * normalised (NEXT-1; not a geometric normal, Q7).
+ * depth: [H][W] double; out: [3][H][W] double (SoA).                        */
+ORC_API int orc_normals_f64_ex(const double* D, int W, int H,
+                               double fx, double fy, double cx, double cy, int mode,
+                               double* out)
 {
     if (!D || !out || W < 1 || H < 1) return -1;
     size_t n = (size_t)W * H;
@@ -119,8 +141,14 @@ ORC_API int orc_normals_f64(const double* D, int W, int H,
                          + (Z(vp, up) - Z(vm, up))) / 8.0;
             double z = Z(v, u);
 #undef Z
-            double mx = fx * gx, my = fy * gy;
-            double mz = -(z + ((double)u - cx) * gx + ((double)v - cy) * gy);
+            double mx, my, mz;
+            if (mode == ORC_NORMALS_AS_PRINTED) {
+                /* Eq. 2 / Alg. 1 ℓ11 taken literally: n = -K^-1 [Gx, Gy, 1]^T */
+                mx = -(gx - cx) / fx; my = -(gy - cy) / fy; mz = -1.0;
+            } else {
+                mx = fx * gx; my = fy * gy;
+                mz = -(z + ((double)u - cx) * gx + ((double)v - cy) * gy);
+            }
             double len = sqrt(mx * mx + my * my + mz * mz);
             if (!(len > 0.0) || !isfinite(len)) { out[p] = 0.0; out[n + p] = 0.0; out[2 * n + p] = 0.0; continue; }
             out[p] = mx / len; out[n + p] = my / len; out[2 * n + p] = mz / len;
@@ -129,18 +157,30 @@ ORC_API int orc_normals_f64(const double* D, int W, int H,
     return 0;
 }
 
+ORC_API int orc_normals_f64(const double* D, int W, int H,
+                            double fx, double fy, double cx, double cy, double* out)
+{
+    return orc_normals_f64_ex(D, W, H, fx, fy, cx, cy, ORC_NORMALS_GEOMETRIC, out);
+}
+
 /* f32-depth entry (the ABI's input type): promotes to double, then as above. */
-ORC_API int orc_normals(const float* depth, int W, int H,
-                        double fx, double fy, double cx, double cy, double* out)
+ORC_API int orc_normals_ex(const float* depth, int W, int H,
+                           double fx, double fy, double cx, double cy, int mode, double* out)
 {
     if (!depth) return -1;
     size_t n = (size_t)W * H;
     double* D = (double*)malloc(n * sizeof(double));
     if (!D) return -1;
     for (size_t p = 0; p < n; ++p) D[p] = (double)depth[p];
-    int rc = orc_normals_f64(D, W, H, fx, fy, cx, cy, out);
+    int rc = orc_normals_f64_ex(D, W, H, fx, fy, cx, cy, mode, out);
     free(D);
     return rc;
+}
+
+ORC_API int orc_normals(const float* depth, int W, int H,
+                        double fx, double fy, double cx, double cy, double* out)
+{
+    return orc_normals_ex(depth, W, H, fx, fy, cx, cy, ORC_NORMALS_GEOMETRIC, out);
 }
 
 /* Sobel gradients alone (the Gx, Gy of Alg. 1 ℓ10), same convention as above;

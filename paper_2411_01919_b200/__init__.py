@@ -28,6 +28,8 @@ _lib = ctypes.CDLL(LIB_PATH)
 STATUS_OK, STATUS_REJECTED, STATUS_TOO_FEW, STATUS_DEGENERATE = 0, 1, 2, 3
 SAMPLER_PHILOX, SAMPLER_ENUMERATE = 0, 1
 SELECT_COUNT, SELECT_ERROR = 0, 1
+ADF_ALG1, ADF_DIVERGENCE = 0, 1
+NORMALS_GEOMETRIC, NORMALS_AS_PRINTED = 0, 1
 PLANE_WORDS = 12          # sizeof(pm_plane) / 4
 
 
@@ -36,7 +38,7 @@ class pm_intrinsics(ctypes.Structure):
 
 
 class pm_adf_options(ctypes.Structure):
-    _fields_ = [("iters_per_pass", ctypes.c_int32)]
+    _fields_ = [("iters_per_pass", ctypes.c_int32), ("scheme", ctypes.c_int32), ("normals_mode", ctypes.c_int32)]
 
 
 class pm_ransac_options(ctypes.Structure):
@@ -64,6 +66,7 @@ _lib.pm_adf_filter_ex.argtypes = [_P, _P, _I32, _I32, _I32, _KP, _F32, _F32, _I3
                                   ctypes.POINTER(pm_adf_options), _P]
 _lib.pm_normals_from_depth.argtypes = [_P, _I32, _I32, _KP, _P, _P]
 _lib.pm_normals_from_depth_batched.argtypes = [_P, _I32, _I32, _I32, _KP, _P, _P]
+_lib.pm_normals_from_depth_ex.argtypes = [_P, _I32, _I32, _I32, _KP, _I32, _P, _P]
 _lib.pm_ransac_planes.argtypes = [_P, _I32, _I32, _KP, _P, _I32, _I32, _F32, _U64, _P, _P, _SZ, _P]
 _lib.pm_ransac_planes_batched.argtypes = [_P, _I32, _I32, _I32, _U32, _KP, _P, _I32, _I32, _F32, _U64,
                                           _P, _P, _SZ, _P]
@@ -72,12 +75,12 @@ _lib.pm_ransac_planes_ex.argtypes = [_P, _I32, _I32, _I32, _U32, _KP, _P, _I32, 
 _lib.pm_process_frames.argtypes = [_P, _P, _I32, _I32, _I32, _U32, _KP, _F32, _F32, _I32, _I32, _I32, _F32,
                                    _U64, _P, _P, _P, _P, _SZ, _P]
 for _fn in ("pm_adf_filter", "pm_adf_filter_batched", "pm_adf_filter_ex", "pm_normals_from_depth",
-            "pm_normals_from_depth_batched", "pm_ransac_planes", "pm_ransac_planes_batched",
-            "pm_ransac_planes_ex", "pm_process_frames"):
+            "pm_normals_from_depth_batched", "pm_normals_from_depth_ex", "pm_ransac_planes",
+            "pm_ransac_planes_batched", "pm_ransac_planes_ex", "pm_process_frames"):
     getattr(_lib, _fn).restype = ctypes.c_int
 
 EXPORTED = ("pm_adf_filter", "pm_adf_filter_batched", "pm_adf_filter_ex", "pm_adf_workspace_bytes",
-            "pm_normals_from_depth", "pm_normals_from_depth_batched", "pm_ransac_planes",
+            "pm_normals_from_depth", "pm_normals_from_depth_batched", "pm_normals_from_depth_ex", "pm_ransac_planes",
             "pm_ransac_planes_batched", "pm_ransac_planes_ex", "pm_ransac_workspace_bytes",
             "pm_process_frames", "pm_pipeline_workspace_bytes", "pm_pipeline_kernel_launches",
             "pm_status_string", "pm_version")
@@ -142,7 +145,7 @@ def pipeline_workspace_bytes(W: int, H: int, n_regions: int, n_hyp: int, n_frame
 
 def adf_filter(depth: torch.Tensor, K, lam: float, kappa: float, iters: int, normals: bool = True,
                iters_per_pass: int = 0, out: torch.Tensor = None, normals_out: torch.Tensor = None,
-               workspace: torch.Tensor = None):
+               workspace: torch.Tensor = None, scheme: int = ADF_ALG1, normals_mode: int = NORMALS_GEOMETRIC):
     """Alg. 1 on [H, W] or [B, H, W] f32 depth (metres, CUDA).
     Returns (I_smooth, normals [.., 3, H, W] or None)."""
     B, H, W = _frames(depth, torch.float32)
@@ -152,20 +155,20 @@ def adf_filter(depth: torch.Tensor, K, lam: float, kappa: float, iters: int, nor
         shape = (3, H, W) if depth.dim() == 2 else (B, 3, H, W)
         nrm = torch.empty(shape, dtype=torch.float32, device=depth.device) if normals_out is None else normals_out
     ws = workspace if workspace is not None else _workspace(adf_workspace_bytes(W, H, B), depth.device)
-    opt = pm_adf_options(int(iters_per_pass))
+    opt = pm_adf_options(int(iters_per_pass), int(scheme), int(normals_mode))
     _check(_lib.pm_adf_filter_ex(depth.data_ptr(), out.data_ptr(), W, H, B, ctypes.byref(_K(K)), float(lam),
                                  float(kappa), int(iters), nrm.data_ptr() if nrm is not None else None,
                                  ws.data_ptr(), ws.numel(), ctypes.byref(opt), _stream(depth)))
     return out, nrm
 
 
-def normals_from_depth(depth: torch.Tensor, K, out: torch.Tensor = None) -> torch.Tensor:
+def normals_from_depth(depth: torch.Tensor, K, out: torch.Tensor = None, mode: int = NORMALS_GEOMETRIC) -> torch.Tensor:
     """Alg. 1 ℓ9-13 on [H, W] or [B, H, W] f32 depth -> [.., 3, H, W]."""
     B, H, W = _frames(depth, torch.float32)
     shape = (3, H, W) if depth.dim() == 2 else (B, 3, H, W)
     out = torch.empty(shape, dtype=torch.float32, device=depth.device) if out is None else out
-    _check(_lib.pm_normals_from_depth_batched(depth.data_ptr(), W, H, B, ctypes.byref(_K(K)), out.data_ptr(),
-                                              _stream(depth)))
+    _check(_lib.pm_normals_from_depth_ex(depth.data_ptr(), W, H, B, ctypes.byref(_K(K)), int(mode), out.data_ptr(),
+                                         _stream(depth)))
     return out
 
 

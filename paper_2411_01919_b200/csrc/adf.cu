@@ -41,7 +41,12 @@ constexpr int kMaxItersPerPass = 16;
 struct AdfParams {
     float kc;         // -log2(e) / (4 kappa^2)
     float l2lam;      // log2(lambda): lambda * c = 2^(kc * g2 + log2(lambda))
+    float kd;         // -log2(e) / kappa^2 (divergence scheme: c(d) = 2^(kd d^2))
+    float lam;
     float fx, fy, cx, cy;
+    float ifx, ify;   // 1/fx, 1/fy (Eq. 2 as printed)
+    int scheme;       // PM_ADF_ALG1 | PM_ADF_DIVERGENCE
+    int nmode;        // PM_NORMALS_GEOMETRIC | PM_NORMALS_AS_PRINTED
 };
 
 // Alg. 1 ℓ4-6 at a valid centre C with neighbour values N, S, W, E (already
@@ -60,8 +65,21 @@ PM_DEVINL float adf_cell(float C, float N, float S, float W, float E, float kc, 
     return __fmaf_rn(lc, lap, C);
 }
 
-template <bool CHECK>
-PM_DEVINL float cell(float C, float N, float S, float W, float E, float kc, float l2lam) {
+// Eq. 1 as the 4-flux Perona-Malik scheme (NEXT-1, reading Q1):
+//   I' = C + lambda * ((c(dN) dN + c(dS) dS) + (c(dW) dW + c(dE) dE)),
+//   dX = X - C, c(d) = exp(-(d / k)^2) = 2^(kd d^2)
+PM_DEVINL float adf_cell_div(float C, float N, float S, float W, float E, float kd, float lam) {
+    const float dn = __fsub_rn(N, C), ds = __fsub_rn(S, C);
+    const float dw = __fsub_rn(W, C), de = __fsub_rn(E, C);
+    const float fn = __fmul_rn(ex2_approx(__fmul_rn(__fmul_rn(dn, dn), kd)), dn);
+    const float fs = __fmul_rn(ex2_approx(__fmul_rn(__fmul_rn(ds, ds), kd)), ds);
+    const float fw = __fmul_rn(ex2_approx(__fmul_rn(__fmul_rn(dw, dw), kd)), dw);
+    const float fe = __fmul_rn(ex2_approx(__fmul_rn(__fmul_rn(de, de), kd)), de);
+    return __fmaf_rn(lam, __fadd_rn(__fadd_rn(fn, fs), __fadd_rn(fw, fe)), C);
+}
+
+template <bool CHECK, bool DIV>
+PM_DEVINL float cell(float C, float N, float S, float W, float E, const AdfParams& p) {
     if (CHECK) {
         if (!valid_depth(C)) return C;                 // invalid pixels never change
         N = valid_depth(N) ? N : C;
@@ -69,7 +87,7 @@ PM_DEVINL float cell(float C, float N, float S, float W, float E, float kc, floa
         W = valid_depth(W) ? W : C;
         E = valid_depth(E) ? E : C;
     }
-    return adf_cell(C, N, S, W, E, kc, l2lam);
+    return DIV ? adf_cell_div(C, N, S, W, E, p.kd, p.lam) : adf_cell(C, N, S, W, E, p.kc, p.l2lam);
 }
 
 // Shared tile: kSW = 128 columns (four 32-lane column groups) x SH rows; the
@@ -83,9 +101,9 @@ struct Box { int ix0, ix1, iy0, iy1; };
 // One Jacobi sweep over smem rows [t, SH - t) x columns [PAD + t, kSW - PAD - t)
 // (PAD = unused alignment columns), clipped to the image.  Warp w walks
 // column group (w & 3), row half (w >> 2).
-template <int SH, int PAD, bool CHECK>
+template <int SH, int PAD, bool CHECK, bool DIV>
 PM_DEVINL void sweep(const float* __restrict__ cur, float* __restrict__ nxt, int t, const Box& b,
-                     float kc, float l2lam) {
+                     const AdfParams& p) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     constexpr int kParts = kWarps / 4;
     const int x = (warp & 3) * 32 + lane;
@@ -110,12 +128,12 @@ PM_DEVINL void sweep(const float* __restrict__ cur, float* __restrict__ nxt, int
         const float S = col[(y + 1) * kSW];
         const float W = colW[y * kSW];
         const float E = colE[y * kSW];
-        ocol[y * kSW] = cell<CHECK>(C, N, S, W, E, kc, l2lam);
+        ocol[y * kSW] = cell<CHECK, DIV>(C, N, S, W, E, p);
         N = C;
         C = S;
     }
     if (ye > ylast)                             // last image row: S = C
-        ocol[y * kSW] = cell<CHECK>(C, N, C, colW[y * kSW], colE[y * kSW], kc, l2lam);
+        ocol[y * kSW] = cell<CHECK, DIV>(C, N, C, colW[y * kSW], colE[y * kSW], p);
 }
 
 // Same sweep with two horizontally adjacent cells per thread (columns x, x+1,
@@ -126,9 +144,9 @@ PM_DEVINL void sweep(const float* __restrict__ cur, float* __restrict__ nxt, int
 // entirely inside or outside the image.  A pair straddling the sweep region's
 // edge also updates its outer cell; that cell lies outside every later
 // region and is never read again.
-template <int SH, int PAD, bool CHECK>
+template <int SH, int PAD, bool CHECK, bool DIV>
 PM_DEVINL void sweep_pairs(const float* __restrict__ cur, float* __restrict__ nxt, int t, const Box& b,
-                           float kc, float l2lam) {
+                           const AdfParams& p) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     constexpr int kParts = kWarps / 2;
     const int x = ((warp & 1) * 32 + lane) * 2;
@@ -155,8 +173,8 @@ PM_DEVINL void sweep_pairs(const float* __restrict__ cur, float* __restrict__ nx
         const float W = colW[y * kSW];
         const float E = colE[y * kSW];
         float2 o;
-        o.x = cell<CHECK>(C.x, N.x, S.x, W, C.y, kc, l2lam);
-        o.y = cell<CHECK>(C.y, N.y, S.y, C.x, E, kc, l2lam);
+        o.x = cell<CHECK, DIV>(C.x, N.x, S.x, W, C.y, p);
+        o.y = cell<CHECK, DIV>(C.y, N.y, S.y, C.x, E, p);
         *reinterpret_cast<float2*>(ocol + y * kSW) = o;
         N = C;
         C = S;
@@ -165,8 +183,8 @@ PM_DEVINL void sweep_pairs(const float* __restrict__ cur, float* __restrict__ nx
         const float W = colW[y * kSW];
         const float E = colE[y * kSW];
         float2 o;
-        o.x = cell<CHECK>(C.x, N.x, C.x, W, C.y, kc, l2lam);
-        o.y = cell<CHECK>(C.y, N.y, C.y, C.x, E, kc, l2lam);
+        o.x = cell<CHECK, DIV>(C.x, N.x, C.x, W, C.y, p);
+        o.y = cell<CHECK, DIV>(C.y, N.y, C.y, C.x, E, p);
         *reinterpret_cast<float2*>(ocol + y * kSW) = o;
     }
 }
@@ -187,9 +205,16 @@ PM_DEVINL float3 sobel_normal(const float z[3][3], float u, float v, const AdfPa
     const float gy = __fmul_rn(__fadd_rn(__fadd_rn(__fsub_rn(z[2][0], z[0][0]),
                                                    __fmul_rn(2.0f, __fsub_rn(z[2][1], z[0][1]))),
                                          __fsub_rn(z[2][2], z[0][2])), 0.125f);
-    const float mx = __fmul_rn(p.fx, gx);
-    const float my = __fmul_rn(p.fy, gy);
-    const float mz = -__fmaf_rn(__fsub_rn(v, p.cy), gy, __fmaf_rn(__fsub_rn(u, p.cx), gx, z[1][1]));
+    float mx, my, mz;
+    if (p.nmode == PM_NORMALS_AS_PRINTED) {      // Eq. 2 literally: -K^-1 [Gx, Gy, 1]^T (NEXT-1)
+        mx = -__fmul_rn(__fsub_rn(gx, p.cx), p.ifx);
+        my = -__fmul_rn(__fsub_rn(gy, p.cy), p.ify);
+        mz = -1.0f;
+    } else {
+        mx = __fmul_rn(p.fx, gx);
+        my = __fmul_rn(p.fy, gy);
+        mz = -__fmaf_rn(__fsub_rn(v, p.cy), gy, __fmaf_rn(__fsub_rn(u, p.cx), gx, z[1][1]));
+    }
     const float ss = __fmaf_rn(mx, mx, __fmaf_rn(my, my, __fmul_rn(mz, mz)));
     if (!(ss > 0.0f) || !(ss <= FLT_MAX)) return make_float3(0.f, 0.f, 0.f);
     const float inv = rsqrtf(ss);
@@ -277,17 +302,17 @@ adf_pass_kernel(const float* __restrict__ src, float* __restrict__ dst, float* _
     float* cur = buf0;
     float* nxt = buf1;
     const bool pairs = ((b.ix0 | b.ix1) & 1) == 0;
+    const bool div = p.scheme == PM_ADF_DIVERGENCE;
     for (int t = 1; t <= iters; ++t) {
-        if (pairs) {
-            if (all_valid)
-                sweep_pairs<SH, PAD, false>(cur, nxt, t, b, p.kc, p.l2lam);
-            else
-                sweep_pairs<SH, PAD, true>(cur, nxt, t, b, p.kc, p.l2lam);
-        } else if (all_valid) {
-            sweep<SH, PAD, false>(cur, nxt, t, b, p.kc, p.l2lam);
+#define PM_SWEEP(FN, CK, DV) FN<SH, PAD, CK, DV>(cur, nxt, t, b, p)
+        if (!div) {
+            if (pairs) { if (all_valid) PM_SWEEP(sweep_pairs, false, false); else PM_SWEEP(sweep_pairs, true, false); }
+            else { if (all_valid) PM_SWEEP(sweep, false, false); else PM_SWEEP(sweep, true, false); }
         } else {
-            sweep<SH, PAD, true>(cur, nxt, t, b, p.kc, p.l2lam);
+            if (pairs) { if (all_valid) PM_SWEEP(sweep_pairs, false, true); else PM_SWEEP(sweep_pairs, true, true); }
+            else { if (all_valid) PM_SWEEP(sweep, false, true); else PM_SWEEP(sweep, true, true); }
         }
+#undef PM_SWEEP
         __syncthreads();
         float* tmp = cur; cur = nxt; nxt = tmp;
     }
@@ -424,21 +449,27 @@ int adf_default_iters_per_pass() { return 4; }
 
 size_t adf_flags_offset(int W, int H, int B) { return (sizeof(float) * (size_t)B * W * H + 255) & ~(size_t)255; }
 
-static AdfParams make_params(const pm_intrinsics* K, float lam, float kappa) {
+static AdfParams make_params(const pm_intrinsics* K, float lam, float kappa, int scheme, int nmode) {
     AdfParams p;
     p.kc = (float)(-1.4426950408889634 / (4.0 * (double)kappa * (double)kappa));
     p.l2lam = (float)log2((double)lam);
+    p.kd = (float)(-1.4426950408889634 / ((double)kappa * (double)kappa));
+    p.lam = lam;
     p.fx = K ? K->fx : 1.f;
     p.fy = K ? K->fy : 1.f;
     p.cx = K ? K->cx : 0.f;
     p.cy = K ? K->cy : 0.f;
+    p.ifx = 1.0f / p.fx;
+    p.ify = 1.0f / p.fy;
+    p.scheme = scheme;
+    p.nmode = nmode;
     return p;
 }
 
 cudaError_t adf_run(const float* in, float* out, float* normals, float* ws, int W, int H, int B,
                     const pm_intrinsics* K, float lam, float kappa, int iters, int iters_per_pass,
-                    cudaStream_t stream) {
-    const AdfParams p = make_params(K, lam, kappa);
+                    int scheme, int nmode, cudaStream_t stream) {
+    const AdfParams p = make_params(K, lam, kappa, scheme, nmode);
     int T = iters_per_pass > 0 ? iters_per_pass : adf_default_iters_per_pass();
     if (T > kMaxItersPerPass) T = kMaxItersPerPass;
     if (iters == 0) {   // N = 0: I_smooth = I (Alg. 1 ℓ1); normals of the input
@@ -470,8 +501,8 @@ cudaError_t adf_run(const float* in, float* out, float* normals, float* ws, int 
 }
 
 cudaError_t normals_run(const float* depth, float* normals, int W, int H, int B,
-                        const pm_intrinsics* K, cudaStream_t stream) {
-    const AdfParams p = make_params(K, 0.25f, 1.0f);
+                        const pm_intrinsics* K, int nmode, cudaStream_t stream) {
+    const AdfParams p = make_params(K, 0.25f, 1.0f, PM_ADF_ALG1, nmode);
     return launch_pass(depth, nullptr, normals, W, H, B, 0, true, p, stream);
 }
 

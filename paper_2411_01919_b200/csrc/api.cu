@@ -47,7 +47,9 @@ pm_status cuda_status(cudaError_t e) { return e == cudaSuccess ? PM_OK : PM_ERR_
 
 pm_status adf_impl(const float* in, float* out, int32_t W, int32_t H, int32_t B, const pm_intrinsics* K,
                    float lam, float kappa, int32_t iters, float* normals, void* ws, size_t ws_bytes,
-                   int32_t iters_per_pass, cudaStream_t stream) {
+                   int32_t iters_per_pass, int32_t scheme, int32_t nmode, cudaStream_t stream) {
+    if (scheme != PM_ADF_ALG1 && scheme != PM_ADF_DIVERGENCE) return PM_ERR_INVALID_ARGUMENT;
+    if (nmode != PM_NORMALS_GEOMETRIC && nmode != PM_NORMALS_AS_PRINTED) return PM_ERR_INVALID_ARGUMENT;
     if (!in || !out || !dims_ok(W, H, B) || iters < 0) return PM_ERR_INVALID_ARGUMENT;
     if (!(lam > 0.0f && lam <= 0.25f) || !finite_pos(kappa)) return PM_ERR_INVALID_ARGUMENT;
     if (normals && !intrinsics_ok(K)) return PM_ERR_INVALID_ARGUMENT;
@@ -62,7 +64,7 @@ pm_status adf_impl(const float* in, float* out, int32_t W, int32_t H, int32_t B,
     if (needs_ws && (overlap(ws, bytes, in, bytes) || overlap(ws, bytes, out, bytes))) return PM_ERR_INVALID_ARGUMENT;
     if (cudaError_t e = setup(); e != cudaSuccess) return PM_ERR_CUDA;
     return cuda_status(pm::adf_run(in, out, normals, (float*)ws, W, H, B, K, lam, kappa, iters,
-                                   iters_per_pass, stream));
+                                   iters_per_pass, scheme, nmode, stream));
 }
 
 pm_status ransac_impl(const float* depth, int32_t W, int32_t H, int32_t B, uint32_t first_frame,
@@ -115,7 +117,7 @@ PM_API pm_status pm_adf_filter(const float* depth_in, float* depth_out, int32_t 
                                const pm_intrinsics* K, float lambda, float kappa, int32_t iters,
                                float* normals_out, void* workspace, size_t ws_bytes, pm_stream_t stream) {
     return adf_impl(depth_in, depth_out, W, H, 1, K, lambda, kappa, iters, normals_out, workspace,
-                    ws_bytes, 0, (cudaStream_t)stream);
+                    ws_bytes, 0, PM_ADF_ALG1, PM_NORMALS_GEOMETRIC, (cudaStream_t)stream);
 }
 
 PM_API pm_status pm_adf_filter_batched(const float* depth_in, float* depth_out, int32_t W, int32_t H,
@@ -123,7 +125,7 @@ PM_API pm_status pm_adf_filter_batched(const float* depth_in, float* depth_out, 
                                        float kappa, int32_t iters, float* normals_out, void* workspace,
                                        size_t ws_bytes, pm_stream_t stream) {
     return adf_impl(depth_in, depth_out, W, H, n_frames, K, lambda, kappa, iters, normals_out, workspace,
-                    ws_bytes, 0, (cudaStream_t)stream);
+                    ws_bytes, 0, PM_ADF_ALG1, PM_NORMALS_GEOMETRIC, (cudaStream_t)stream);
 }
 
 PM_API pm_status pm_adf_filter_ex(const float* depth_in, float* depth_out, int32_t W, int32_t H,
@@ -131,7 +133,8 @@ PM_API pm_status pm_adf_filter_ex(const float* depth_in, float* depth_out, int32
                                   int32_t iters, float* normals_out, void* workspace, size_t ws_bytes,
                                   const pm_adf_options* opt, pm_stream_t stream) {
     return adf_impl(depth_in, depth_out, W, H, n_frames, K, lambda, kappa, iters, normals_out, workspace,
-                    ws_bytes, opt ? opt->iters_per_pass : 0, (cudaStream_t)stream);
+                    ws_bytes, opt ? opt->iters_per_pass : 0, opt ? opt->scheme : PM_ADF_ALG1,
+                    opt ? opt->normals_mode : PM_NORMALS_GEOMETRIC, (cudaStream_t)stream);
 }
 
 PM_API pm_status pm_normals_from_depth(const float* depth, int32_t W, int32_t H, const pm_intrinsics* K,
@@ -142,11 +145,18 @@ PM_API pm_status pm_normals_from_depth(const float* depth, int32_t W, int32_t H,
 PM_API pm_status pm_normals_from_depth_batched(const float* depth, int32_t W, int32_t H, int32_t n_frames,
                                                const pm_intrinsics* K, float* normals_out,
                                                pm_stream_t stream) {
+    return pm_normals_from_depth_ex(depth, W, H, n_frames, K, PM_NORMALS_GEOMETRIC, normals_out, stream);
+}
+
+PM_API pm_status pm_normals_from_depth_ex(const float* depth, int32_t W, int32_t H, int32_t n_frames,
+                                          const pm_intrinsics* K, int32_t mode, float* normals_out,
+                                          pm_stream_t stream) {
     if (!depth || !normals_out || !dims_ok(W, H, n_frames) || !intrinsics_ok(K)) return PM_ERR_INVALID_ARGUMENT;
+    if (mode != PM_NORMALS_GEOMETRIC && mode != PM_NORMALS_AS_PRINTED) return PM_ERR_INVALID_ARGUMENT;
     const size_t bytes = sizeof(float) * (size_t)n_frames * W * H;
     if (overlap(depth, bytes, normals_out, 3 * bytes)) return PM_ERR_INVALID_ARGUMENT;
     if (cudaError_t e = setup(); e != cudaSuccess) return PM_ERR_CUDA;
-    return cuda_status(pm::normals_run(depth, normals_out, W, H, n_frames, K, (cudaStream_t)stream));
+    return cuda_status(pm::normals_run(depth, normals_out, W, H, n_frames, K, mode, (cudaStream_t)stream));
 }
 
 PM_API size_t pm_ransac_workspace_bytes(int32_t W, int32_t H, int32_t n_regions, int32_t n_hyp,
@@ -196,7 +206,7 @@ PM_API pm_status pm_process_frames(const float* depth_in, const int32_t* region_
     if (!depth_out || !normals_out) return PM_ERR_INVALID_ARGUMENT;
     if (ws_bytes < pm_pipeline_workspace_bytes(W, H, n_regions, n_hyp, n_frames)) return PM_ERR_WORKSPACE;
     pm_status s = adf_impl(depth_in, depth_out, W, H, n_frames, K, lambda, kappa, iters, normals_out, workspace,
-                           ws_bytes, 0, (cudaStream_t)stream);
+                           ws_bytes, 0, PM_ADF_ALG1, PM_NORMALS_GEOMETRIC, (cudaStream_t)stream);
     if (s != PM_OK) return s;
     return ransac_impl(depth_out, W, H, n_frames, first_frame_id, K, region_labels, n_regions, n_hyp,
                        inlier_thresh, seed, planes_out, workspace, ws_bytes, nullptr, (cudaStream_t)stream);

@@ -16,9 +16,9 @@ size_t adf_flags_offset(int W, int H, int B);
 // in -> out (B frames); ws: B*H*W floats (used when >= 2 passes); normals nullable.
 cudaError_t adf_run(const float* in, float* out, float* normals, float* ws, int W, int H, int B,
                     const pm_intrinsics* K, float lam, float kappa, int iters, int iters_per_pass,
-                    cudaStream_t stream);
+                    int scheme, int nmode, cudaStream_t stream);
 cudaError_t normals_run(const float* depth, float* normals, int W, int H, int B,
-                        const pm_intrinsics* K, cudaStream_t stream);
+                        const pm_intrinsics* K, int nmode, cudaStream_t stream);
 
 // ---- compact.cu / ransac.cu
 struct Sums;

@@ -286,3 +286,23 @@ def test_bench_configuration_sampled(pm):
         ok = ref["status"] <= 1
         assert np.abs(planes.n[i].cpu().numpy()[ok] - ref["n"][ok]).max() <= REFIT_TOL
         assert np.abs(planes.centroid[i].cpu().numpy()[ok] - ref["centroid"][ok]).max() <= REFIT_TOL
+
+
+# -------------------------------------------------- NEXT-1 paper-literal modes
+@pytest.mark.parametrize("name,kw", [("C1n", {}), ("C2", {}), ("C2", {"holes": 0.01}), ("C2", {"W": 333, "H": 251})])
+def test_divergence_scheme_and_printed_normals(pm, name, kw):
+    fr = scenegen.make_config(name, **kw)
+    d_in = fr["depth"].numpy()
+    d_out, nrm = pm.adf_filter(fr["depth"].to(DEV), fr["K"], fr["lam"], fr["kappa"], fr["iters"],
+                               scheme=pm.ADF_DIVERGENCE, normals_mode=pm.NORMALS_AS_PRINTED)
+    torch.cuda.synchronize()
+    d_gpu = d_out.cpu().numpy()
+    _check_depth(d_gpu, d_in, oracle.adf(d_in, fr["lam"], fr["kappa"], fr["iters"], scheme=oracle.ADF_DIVERGENCE))
+    _check_normals(nrm.cpu().numpy(), oracle.normals(d_gpu, fr["K"], mode=oracle.NORMALS_AS_PRINTED))
+    n2 = pm.normals_from_depth(fr["depth"].to(DEV), fr["K"], mode=pm.NORMALS_AS_PRINTED)
+    torch.cuda.synchronize()
+    _check_normals(n2.cpu().numpy(), oracle.normals(d_in, fr["K"], mode=oracle.NORMALS_AS_PRINTED))
+    # blocking invariance holds for this scheme too
+    d2, _ = pm.adf_filter(fr["depth"].to(DEV), fr["K"], fr["lam"], fr["kappa"], fr["iters"], iters_per_pass=3,
+                          scheme=pm.ADF_DIVERGENCE, normals=False)
+    assert torch.equal(d2.cpu(), d_out.cpu())
