@@ -234,7 +234,7 @@ __host__ __device__ constexpr int tile_w() { return kSW - 2 * halo_x<R>(); }
 
 // One pass of `iters` sweeps; halo R = iters (+1 when the normals are fused).
 //   src [B][H][W] -> dst [B][H][W] (if dst) and normals [B][3][H][W] (if normals).
-template <int R>
+template <int R, bool DIV>
 __global__ void __launch_bounds__(kThreads, 2)
 adf_pass_kernel(const float* __restrict__ src, float* __restrict__ dst, float* __restrict__ normals,
                 int W, int H, int iters, AdfParams p, const __grid_constant__ CUtensorMap tmap, int use_tma,
@@ -302,16 +302,10 @@ adf_pass_kernel(const float* __restrict__ src, float* __restrict__ dst, float* _
     float* cur = buf0;
     float* nxt = buf1;
     const bool pairs = ((b.ix0 | b.ix1) & 1) == 0;
-    const bool div = p.scheme == PM_ADF_DIVERGENCE;
     for (int t = 1; t <= iters; ++t) {
-#define PM_SWEEP(FN, CK, DV) FN<SH, PAD, CK, DV>(cur, nxt, t, b, p)
-        if (!div) {
-            if (pairs) { if (all_valid) PM_SWEEP(sweep_pairs, false, false); else PM_SWEEP(sweep_pairs, true, false); }
-            else { if (all_valid) PM_SWEEP(sweep, false, false); else PM_SWEEP(sweep, true, false); }
-        } else {
-            if (pairs) { if (all_valid) PM_SWEEP(sweep_pairs, false, true); else PM_SWEEP(sweep_pairs, true, true); }
-            else { if (all_valid) PM_SWEEP(sweep, false, true); else PM_SWEEP(sweep, true, true); }
-        }
+#define PM_SWEEP(FN, CK) FN<SH, PAD, CK, DIV>(cur, nxt, t, b, p)
+        if (pairs) { if (all_valid) PM_SWEEP(sweep_pairs, false); else PM_SWEEP(sweep_pairs, true); }
+        else { if (all_valid) PM_SWEEP(sweep, false); else PM_SWEEP(sweep, true); }
 #undef PM_SWEEP
         __syncthreads();
         float* tmp = cur; cur = nxt; nxt = tmp;
@@ -395,8 +389,9 @@ using PassFn = void (*)(const float*, float*, float*, int, int, int, AdfParams, 
 
 template <int R>
 struct PassTable {
-    static void fill(PassFn* fns, size_t* smem, int* tw) {
-        fns[R] = adf_pass_kernel<R>;
+    static void fill(PassFn (*fns)[2], size_t* smem, int* tw) {
+        fns[R][0] = adf_pass_kernel<R, false>;
+        fns[R][1] = adf_pass_kernel<R, true>;
         smem[R] = pass_smem_bytes<R>();
         tw[R] = tile_w<R>();
         PassTable<R - 1>::fill(fns, smem, tw);
@@ -404,11 +399,11 @@ struct PassTable {
 };
 template <>
 struct PassTable<0> {
-    static void fill(PassFn*, size_t*, int*) {}
+    static void fill(PassFn (*)[2], size_t*, int*) {}
 };
 
 struct Passes {
-    PassFn fn[kMaxItersPerPass + 2] = {};
+    PassFn fn[kMaxItersPerPass + 2][2] = {};   // [R][scheme == PM_ADF_DIVERGENCE]
     size_t smem[kMaxItersPerPass + 2] = {};
     int tw[kMaxItersPerPass + 2] = {};
     Passes() { PassTable<kMaxItersPerPass + 1>::fill(fn, smem, tw); }
@@ -422,10 +417,12 @@ const Passes& passes() {
 
 cudaError_t adf_setup_attributes() {
     const Passes& P = passes();
-    for (int R = 1; R <= kMaxItersPerPass + 1; ++R) {
-        cudaError_t e = cudaFuncSetAttribute(P.fn[R], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P.smem[R]);
-        if (e != cudaSuccess) return e;
-    }
+    for (int R = 1; R <= kMaxItersPerPass + 1; ++R)
+        for (int d = 0; d < 2; ++d) {
+            cudaError_t e = cudaFuncSetAttribute(P.fn[R][d], cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 (int)P.smem[R]);
+            if (e != cudaSuccess) return e;
+        }
     return cudaSuccess;
 }
 
@@ -442,7 +439,8 @@ static cudaError_t launch_pass(const float* src, float* dst, float* normals, int
     void* args[] = {(void*)&src,  (void*)&dst,  (void*)&normals, (void*)&W,           (void*)&H,
                     (void*)&iters, (void*)&p,   (void*)&tmap,    (void*)&use_tma,     (void*)&frame_flags,
                     (void*)&flag_mode};
-    return cudaLaunchKernel((const void*)P.fn[R], grid, dim3(kThreads), args, P.smem[R], stream);
+    return cudaLaunchKernel((const void*)P.fn[R][p.scheme == PM_ADF_DIVERGENCE ? 1 : 0], grid, dim3(kThreads), args,
+                            P.smem[R], stream);
 }
 
 int adf_default_iters_per_pass() { return 4; }
