@@ -213,6 +213,38 @@ PM_API pm_status pm_process_frames(const float* depth_in, const int32_t* region_
 PM_API size_t pm_pipeline_workspace_bytes(int32_t W, int32_t H, int32_t n_regions, int32_t n_hyp,
                                           int32_t n_frames);
 
+/* ---------------------------------------------------------------------- */
+/* The whole path for frames in HOST memory: chunks of chunk_frames frames
+ * are copied to the device, processed by pm_process_frames and the plane
+ * tables (and, if the pointers are not NULL, the filtered depth [B][H][W] and
+ * normals [B][3][H][W]) copied back, double-buffered so that the copies of
+ * one chunk overlap the kernels of the previous one (the caller's stream plus
+ * one internal copy stream per device, created on first use).  Host buffers
+ * should be pinned (cudaHostAlloc / cudaHostRegister) for the copies to be
+ * asynchronous.  Synchronises before returning.
+ *   depth_host   [B][H][W] in depth_format: PM_DEPTH_F32_M (f32 metres) or
+ *                PM_DEPTH_U16_MM (uint16 millimetres, the sensor's native
+ *                format; 0 = invalid; converted as (float)mm * 1e-3f)
+ *   labels_host  [B][H][W] in label_format: PM_LABELS_I32 (int32, -1 = none) or
+ *                PM_LABELS_U16 (uint16, 0xFFFF = none; n_regions <= 65535)
+ *   planes_host  [B][n_regions] pm_plane (host)
+ *   arena        device memory >= pm_host_pipeline_arena_bytes(...), 256-B aligned.
+ * Other arguments as pm_process_frames. */
+enum { PM_DEPTH_F32_M = 0, PM_DEPTH_U16_MM = 1 };
+enum { PM_LABELS_I32 = 0, PM_LABELS_U16 = 1 };
+PM_API pm_status pm_process_frames_host(const void* depth_host, int32_t depth_format, const void* labels_host,
+                                        int32_t label_format, int32_t W, int32_t H, int32_t n_frames,
+                                        uint32_t first_frame_id, const pm_intrinsics* K, float lambda,
+                                        float kappa, int32_t iters, int32_t n_regions, int32_t n_hyp,
+                                        float inlier_thresh, uint64_t seed, pm_plane* planes_host,
+                                        float* depth_out_host, float* normals_host, int32_t chunk_frames,
+                                        void* arena, size_t arena_bytes, pm_stream_t stream);
+PM_API size_t pm_host_pipeline_arena_bytes(int32_t W, int32_t H, int32_t n_regions, int32_t n_hyp,
+                                           int32_t chunk_frames, int32_t depth_format, int32_t label_format);
+/* uint16 millimetres -> f32 metres (device buffers, n values): m = (float)mm * scale. */
+PM_API pm_status pm_depth_u16_to_metres(const uint16_t* depth_mm, float* depth_m, size_t n, float scale,
+                                        pm_stream_t stream);
+
 /* Number of kernel launches one pm_process_frames call enqueues (for the
  * bench's launch accounting; memsets excluded). */
 PM_API int32_t pm_pipeline_kernel_launches(int32_t iters, int32_t n_regions);

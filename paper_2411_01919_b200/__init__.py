@@ -30,6 +30,8 @@ SAMPLER_PHILOX, SAMPLER_ENUMERATE = 0, 1
 SELECT_COUNT, SELECT_ERROR = 0, 1
 ADF_ALG1, ADF_DIVERGENCE = 0, 1
 NORMALS_GEOMETRIC, NORMALS_AS_PRINTED = 0, 1
+DEPTH_F32_M, DEPTH_U16_MM = 0, 1
+LABELS_I32, LABELS_U16 = 0, 1
 PLANE_WORDS = 12          # sizeof(pm_plane) / 4
 
 
@@ -74,15 +76,22 @@ _lib.pm_ransac_planes_ex.argtypes = [_P, _I32, _I32, _I32, _U32, _KP, _P, _I32, 
                                      ctypes.POINTER(pm_ransac_options), _P]
 _lib.pm_process_frames.argtypes = [_P, _P, _I32, _I32, _I32, _U32, _KP, _F32, _F32, _I32, _I32, _I32, _F32,
                                    _U64, _P, _P, _P, _P, _SZ, _P]
+_lib.pm_process_frames_host.argtypes = [_P, _I32, _P, _I32, _I32, _I32, _I32, _U32, _KP, _F32, _F32, _I32, _I32,
+                                        _I32, _F32, _U64, _P, _P, _P, _I32, _P, _SZ, _P]
+_lib.pm_host_pipeline_arena_bytes.restype = _SZ
+_lib.pm_host_pipeline_arena_bytes.argtypes = [_I32, _I32, _I32, _I32, _I32, _I32, _I32]
+_lib.pm_depth_u16_to_metres.argtypes = [_P, _P, _SZ, _F32, _P]
 for _fn in ("pm_adf_filter", "pm_adf_filter_batched", "pm_adf_filter_ex", "pm_normals_from_depth",
             "pm_normals_from_depth_batched", "pm_normals_from_depth_ex", "pm_ransac_planes",
-            "pm_ransac_planes_batched", "pm_ransac_planes_ex", "pm_process_frames"):
+            "pm_ransac_planes_batched", "pm_ransac_planes_ex", "pm_process_frames", "pm_process_frames_host",
+            "pm_depth_u16_to_metres"):
     getattr(_lib, _fn).restype = ctypes.c_int
 
 EXPORTED = ("pm_adf_filter", "pm_adf_filter_batched", "pm_adf_filter_ex", "pm_adf_workspace_bytes",
             "pm_normals_from_depth", "pm_normals_from_depth_batched", "pm_normals_from_depth_ex", "pm_ransac_planes",
             "pm_ransac_planes_batched", "pm_ransac_planes_ex", "pm_ransac_workspace_bytes",
             "pm_process_frames", "pm_pipeline_workspace_bytes", "pm_pipeline_kernel_launches",
+            "pm_process_frames_host", "pm_host_pipeline_arena_bytes", "pm_depth_u16_to_metres",
             "pm_status_string", "pm_version")
 
 
@@ -258,3 +267,52 @@ def process_frames(depth: torch.Tensor, labels: torch.Tensor, K, lam: float, kap
                                   normals_out.data_ptr(), planes_out.data_ptr(), ws.data_ptr(), ws.numel(),
                                   _stream(depth)))
     return depth_out, normals_out, Planes(planes_out)
+
+
+def host_pipeline_arena_bytes(W: int, H: int, n_regions: int, n_hyp: int, chunk_frames: int,
+                              depth_format: int = DEPTH_F32_M, label_format: int = LABELS_I32) -> int:
+    return int(_lib.pm_host_pipeline_arena_bytes(W, H, n_regions, n_hyp, chunk_frames, depth_format, label_format))
+
+
+def depth_u16_to_metres(depth_mm: torch.Tensor, out: torch.Tensor = None, scale: float = 1e-3) -> torch.Tensor:
+    """uint16 millimetres -> f32 metres on the device (0 stays 0 = invalid)."""
+    if depth_mm.dtype != torch.uint16 or not depth_mm.is_cuda or not depth_mm.is_contiguous():
+        raise PMError("pmap: expected a contiguous CUDA uint16 tensor")
+    out = torch.empty(depth_mm.shape, dtype=torch.float32, device=depth_mm.device) if out is None else out
+    _check(_lib.pm_depth_u16_to_metres(depth_mm.data_ptr(), out.data_ptr(), depth_mm.numel(), float(scale),
+                                       _stream(out)))
+    return out
+
+
+def process_frames_host(depth: torch.Tensor, labels: torch.Tensor, K, lam: float, kappa: float, iters: int,
+                        n_regions: int, n_hyp: int, tau: float, seed: int, first_frame_id: int = 0,
+                        chunk_frames: int = 64, planes_out: torch.Tensor = None, depth_out: torch.Tensor = None,
+                        normals_out: torch.Tensor = None, arena: torch.Tensor = None, device=None):
+    """pm_process_frames_host: CPU (preferably pinned) tensors in, CPU plane
+    table out.  depth: [B, H, W] float32 metres or uint16 millimetres; labels:
+    [B, H, W] int32 or uint16 (0xFFFF = none)."""
+    if depth.is_cuda or labels.is_cuda:
+        raise PMError("pmap: process_frames_host takes host tensors")
+    if depth.dim() != 3 or tuple(labels.shape) != tuple(depth.shape):
+        raise PMError("pmap: expected [B, H, W] depth and labels")
+    dfmt = {torch.float32: DEPTH_F32_M, torch.uint16: DEPTH_U16_MM}.get(depth.dtype)
+    lfmt = {torch.int32: LABELS_I32, torch.uint16: LABELS_U16}.get(labels.dtype)
+    if dfmt is None or lfmt is None or not depth.is_contiguous() or not labels.is_contiguous():
+        raise PMError("pmap: depth float32|uint16, labels int32|uint16, contiguous")
+    B, H, W = depth.shape
+    dev = torch.device("cuda") if device is None else torch.device(device)
+    C = min(int(chunk_frames), B)
+    if arena is None:
+        arena = torch.empty(host_pipeline_arena_bytes(W, H, n_regions, n_hyp, C, dfmt, lfmt), dtype=torch.uint8,
+                            device=dev)
+    planes_out = torch.empty(B, n_regions, PLANE_WORDS, dtype=torch.int32) if planes_out is None else planes_out
+    with torch.cuda.device(dev):
+        stream = torch.cuda.current_stream(dev).cuda_stream
+        _check(_lib.pm_process_frames_host(depth.data_ptr(), dfmt, labels.data_ptr(), lfmt, W, H, B,
+                                           int(first_frame_id), ctypes.byref(_K(K)), float(lam), float(kappa),
+                                           int(iters), int(n_regions), int(n_hyp), float(tau),
+                                           int(seed) & (2**64 - 1), planes_out.data_ptr(),
+                                           depth_out.data_ptr() if depth_out is not None else None,
+                                           normals_out.data_ptr() if normals_out is not None else None, C,
+                                           arena.data_ptr(), arena.numel(), stream))
+    return Planes(planes_out)

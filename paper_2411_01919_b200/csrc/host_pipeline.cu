@@ -1,0 +1,213 @@
+// host_pipeline.cu — the whole path for frames in HOST memory
+// (pm_process_frames_host): chunked, double-buffered H2D / compute / D2H on
+// the caller's stream plus one internal copy stream per device, so the copy
+// of chunk k+1 overlaps the kernels of chunk k.  Sensor-native inputs
+// (uint16 millimetres; uint16 labels) halve the PCIe bytes.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string.h>
+
+#include <mutex>
+
+#include "../../include/pmap.h"
+#include "common.cuh"
+#include "internal.h"
+
+namespace pm {
+
+namespace {
+
+constexpr int kConvThreads = 256;
+
+// Alg. 1 input convention: uint16 millimetres -> f32 metres, 0 stays 0 (invalid)
+__global__ void __launch_bounds__(kConvThreads)
+u16_to_metres_kernel(const uint16_t* __restrict__ mm, float* __restrict__ out, size_t n, float scale) {
+    const size_t i0 = ((size_t)blockIdx.x * kConvThreads + threadIdx.x) * 4;
+    if (i0 + 3 < n && ((reinterpret_cast<uintptr_t>(mm + i0) & 7) == 0)) {
+        const ushort4 v = *reinterpret_cast<const ushort4*>(mm + i0);
+        *reinterpret_cast<float4*>(out + i0) =
+            make_float4(__fmul_rn((float)v.x, scale), __fmul_rn((float)v.y, scale), __fmul_rn((float)v.z, scale),
+                        __fmul_rn((float)v.w, scale));
+        return;
+    }
+    for (size_t i = i0; i < n && i < i0 + 4; ++i) out[i] = __fmul_rn((float)mm[i], scale);
+}
+
+// uint16 labels -> int32, 0xFFFF -> -1 (unlabelled)
+__global__ void __launch_bounds__(kConvThreads)
+u16_labels_kernel(const uint16_t* __restrict__ in, int32_t* __restrict__ out, size_t n) {
+    const size_t i = (size_t)blockIdx.x * kConvThreads + threadIdx.x;
+    if (i < n) out[i] = in[i] == 0xFFFFu ? -1 : (int32_t)in[i];
+}
+
+struct DeviceStreams {
+    cudaStream_t copy = nullptr;
+    cudaEvent_t h2d[2] = {}, done[2] = {}, freed[2] = {};
+    std::mutex mu;            // one host pipeline at a time per device
+    cudaError_t err = cudaSuccess;
+};
+
+DeviceStreams* streams_for_current_device() {
+    static std::mutex g;
+    static DeviceStreams* per_dev[64] = {};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+    std::lock_guard<std::mutex> lk(g);
+    if (!per_dev[dev]) {
+        DeviceStreams* d = new DeviceStreams();
+        d->err = cudaStreamCreateWithFlags(&d->copy, cudaStreamNonBlocking);
+        for (int s = 0; s < 2 && d->err == cudaSuccess; ++s) {
+            d->err = cudaEventCreateWithFlags(&d->h2d[s], cudaEventDisableTiming);
+            if (d->err == cudaSuccess) d->err = cudaEventCreateWithFlags(&d->done[s], cudaEventDisableTiming);
+            if (d->err == cudaSuccess) d->err = cudaEventCreateWithFlags(&d->freed[s], cudaEventDisableTiming);
+        }
+        per_dev[dev] = d;
+    }
+    return per_dev[dev];
+}
+
+size_t a256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+struct Slot {
+    void* raw_depth;      // host-format depth staging (u16) or f32 depth directly
+    void* raw_labels;     // host-format labels (u16) or int32 directly
+    float* depth;         // f32 metres (== raw_depth for f32 input)
+    int32_t* labels;      // int32 (== raw_labels for int32 input)
+    float* depth_out;
+    float* normals;
+    pm_plane* planes;
+    void* ws;
+    size_t ws_bytes;
+};
+
+struct Arena {
+    size_t slot_bytes;
+    Slot slot[2];
+};
+
+Arena arena_layout(void* base, int W, int H, int R, int n_hyp, int C, int depth_fmt, int label_fmt) {
+    Arena a{};
+    const size_t px = (size_t)C * W * H;
+    const size_t ws = pm_pipeline_workspace_bytes(W, H, R, n_hyp, C);
+    size_t o = 0;
+    char* p = (char*)base;
+    for (int s = 0; s < 2; ++s) {
+        auto take = [&](size_t b) { void* q = p ? p + o : nullptr; o += a256(b); return q; };
+        Slot& sl = a.slot[s];
+        sl.depth = (float*)take(sizeof(float) * px);
+        sl.raw_depth = depth_fmt == PM_DEPTH_U16_MM ? take(sizeof(uint16_t) * px) : (void*)sl.depth;
+        sl.labels = (int32_t*)take(sizeof(int32_t) * px);
+        sl.raw_labels = label_fmt == PM_LABELS_U16 ? take(sizeof(uint16_t) * px) : (void*)sl.labels;
+        sl.depth_out = (float*)take(sizeof(float) * px);
+        sl.normals = (float*)take(sizeof(float) * 3 * px);
+        sl.planes = (pm_plane*)take(sizeof(pm_plane) * (size_t)C * (R > 0 ? R : 1));
+        sl.ws = take(ws);
+        sl.ws_bytes = ws;
+    }
+    a.slot_bytes = o / 2;
+    return a;
+}
+
+}  // namespace
+
+}  // namespace pm
+
+extern "C" {
+
+PM_API size_t pm_host_pipeline_arena_bytes(int32_t W, int32_t H, int32_t n_regions, int32_t n_hyp,
+                                           int32_t chunk_frames, int32_t depth_format, int32_t label_format) {
+    if (W < 1 || H < 1 || n_regions < 0 || n_hyp < 1 || chunk_frames < 1) return 0;
+    pm::Arena a = pm::arena_layout(nullptr, W, H, n_regions, n_hyp, chunk_frames, depth_format, label_format);
+    return 2 * a.slot_bytes;
+}
+
+PM_API pm_status pm_depth_u16_to_metres(const uint16_t* depth_mm, float* depth_m, size_t n, float scale,
+                                        pm_stream_t stream) {
+    if (!depth_mm || !depth_m || !(scale > 0.0f)) return PM_ERR_INVALID_ARGUMENT;
+    if (n == 0) return PM_OK;
+    const size_t quads = (n + 3) / 4;
+    pm::u16_to_metres_kernel<<<(unsigned)((quads + pm::kConvThreads - 1) / pm::kConvThreads), pm::kConvThreads, 0,
+                               (cudaStream_t)stream>>>(depth_mm, depth_m, n, scale);
+    return cudaGetLastError() == cudaSuccess ? PM_OK : PM_ERR_CUDA;
+}
+
+PM_API pm_status pm_process_frames_host(const void* depth_host, int32_t depth_format, const void* labels_host,
+                                        int32_t label_format, int32_t W, int32_t H, int32_t n_frames,
+                                        uint32_t first_frame_id, const pm_intrinsics* K, float lambda, float kappa,
+                                        int32_t iters, int32_t n_regions, int32_t n_hyp, float inlier_thresh,
+                                        uint64_t seed, pm_plane* planes_host, float* depth_out_host,
+                                        float* normals_host, int32_t chunk_frames, void* arena, size_t arena_bytes,
+                                        pm_stream_t stream) {
+    using namespace pm;
+    if (!depth_host || !labels_host || !planes_host || chunk_frames < 1 || n_frames < 1)
+        return PM_ERR_INVALID_ARGUMENT;
+    if (depth_format != PM_DEPTH_F32_M && depth_format != PM_DEPTH_U16_MM) return PM_ERR_INVALID_ARGUMENT;
+    if (label_format != PM_LABELS_I32 && label_format != PM_LABELS_U16) return PM_ERR_INVALID_ARGUMENT;
+    if (label_format == PM_LABELS_U16 && n_regions > 65535) return PM_ERR_INVALID_ARGUMENT;
+    const int C = chunk_frames < n_frames ? chunk_frames : n_frames;
+    if (!arena || arena_bytes < pm_host_pipeline_arena_bytes(W, H, n_regions, n_hyp, C, depth_format, label_format) ||
+        ((uintptr_t)arena & 255u))
+        return PM_ERR_WORKSPACE;
+    DeviceStreams* ds = streams_for_current_device();
+    if (!ds || ds->err != cudaSuccess) return PM_ERR_CUDA;
+    std::lock_guard<std::mutex> lk(ds->mu);
+    const Arena A = arena_layout(arena, W, H, n_regions, n_hyp, C, depth_format, label_format);
+    cudaStream_t cs = (cudaStream_t)stream;
+    const size_t frame_px = (size_t)W * H;
+    const size_t dsz = depth_format == PM_DEPTH_U16_MM ? 2 : 4;
+    const size_t lsz = label_format == PM_LABELS_U16 ? 2 : 4;
+    const int n_chunks = (n_frames + C - 1) / C;
+    cudaError_t e = cudaSuccess;
+    // both slots start free
+    for (int s = 0; s < 2 && e == cudaSuccess; ++s) e = cudaEventRecord(ds->freed[s], cs);
+    for (int k = 0; k < n_chunks && e == cudaSuccess; ++k) {
+        const int s = k & 1;
+        const Slot& sl = A.slot[s];
+        const int f0 = k * C;
+        const int nf = (n_frames - f0) < C ? (n_frames - f0) : C;
+        const size_t px = (size_t)nf * frame_px;
+        // H2D on the copy stream once the slot's previous results are out
+        e = cudaStreamWaitEvent(ds->copy, ds->freed[s], 0);
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(sl.raw_depth, (const char*)depth_host + (size_t)f0 * frame_px * dsz, px * dsz,
+                                cudaMemcpyHostToDevice, ds->copy);
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(sl.raw_labels, (const char*)labels_host + (size_t)f0 * frame_px * lsz, px * lsz,
+                                cudaMemcpyHostToDevice, ds->copy);
+        if (e == cudaSuccess) e = cudaEventRecord(ds->h2d[s], ds->copy);
+        // compute on the caller's stream
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, ds->h2d[s], 0);
+        if (e != cudaSuccess) break;
+        if (depth_format == PM_DEPTH_U16_MM) {
+            pm_status st = pm_depth_u16_to_metres((const uint16_t*)sl.raw_depth, sl.depth, px, 1e-3f, stream);
+            if (st != PM_OK) return st;
+        }
+        if (label_format == PM_LABELS_U16) {
+            u16_labels_kernel<<<(unsigned)((px + kConvThreads - 1) / kConvThreads), kConvThreads, 0, cs>>>(
+                (const uint16_t*)sl.raw_labels, sl.labels, px);
+            if ((e = cudaGetLastError()) != cudaSuccess) break;
+        }
+        pm_status st = pm_process_frames(sl.depth, sl.labels, W, H, nf, first_frame_id + (uint32_t)f0, K, lambda,
+                                         kappa, iters, n_regions, n_hyp, inlier_thresh, seed, sl.depth_out,
+                                         sl.normals, sl.planes, sl.ws, sl.ws_bytes, stream);
+        if (st != PM_OK) return st;
+        e = cudaEventRecord(ds->done[s], cs);
+        // D2H of the results on the copy stream; the slot is free afterwards
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(ds->copy, ds->done[s], 0);
+        if (e == cudaSuccess && n_regions > 0)
+            e = cudaMemcpyAsync(planes_host + (size_t)f0 * n_regions, sl.planes, sizeof(pm_plane) * nf * n_regions,
+                                cudaMemcpyDeviceToHost, ds->copy);
+        if (e == cudaSuccess && depth_out_host)
+            e = cudaMemcpyAsync(depth_out_host + (size_t)f0 * frame_px, sl.depth_out, sizeof(float) * px,
+                                cudaMemcpyDeviceToHost, ds->copy);
+        if (e == cudaSuccess && normals_host)
+            e = cudaMemcpyAsync(normals_host + (size_t)f0 * 3 * frame_px, sl.normals, sizeof(float) * 3 * px,
+                                cudaMemcpyDeviceToHost, ds->copy);
+        if (e == cudaSuccess) e = cudaEventRecord(ds->freed[s], ds->copy);
+    }
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ds->copy);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(cs);
+    return e == cudaSuccess ? PM_OK : PM_ERR_CUDA;
+}
+
+}  // extern "C"

@@ -306,3 +306,32 @@ def test_divergence_scheme_and_printed_normals(pm, name, kw):
     d2, _ = pm.adf_filter(fr["depth"].to(DEV), fr["K"], fr["lam"], fr["kappa"], fr["iters"], iters_per_pass=3,
                           scheme=pm.ADF_DIVERGENCE, normals=False)
     assert torch.equal(d2.cpu(), d_out.cpu())
+
+
+def test_host_pipeline_matches_device_pipeline(pm):
+    """pm_process_frames_host (chunked, double-buffered, sensor-native uint16
+    inputs) gives bit-identical plane tables to pm_process_frames on the same
+    frames converted on the device."""
+    B, W, H, R, NH = 5, 160, 120, 16, 32
+    d, lab, K = scenegen.stair_stream(100, B, W, H, R)
+    mm = torch.round(d.double() * 1000).clamp(0, 65535).to(torch.int32).to(torch.uint16)
+    lab16 = torch.where(lab < 0, torch.full_like(lab, 0xFFFF), lab).to(torch.int32).to(torch.uint16)
+    depth_out = torch.empty(B, H, W).pin_memory()
+    normals_out = torch.empty(B, 3, H, W).pin_memory()
+    planes_h = pm.process_frames_host(mm.pin_memory(), lab16.pin_memory(), K, 0.15, 0.03, 20, R, NH, 0.01, 77,
+                                      first_frame_id=100, chunk_frames=2, depth_out=depth_out,
+                                      normals_out=normals_out)
+    dm = pm.depth_u16_to_metres(mm.to(DEV))
+    d_dev, n_dev, planes_d = pm.process_frames(dm, lab.to(DEV), K, 0.15, 0.03, 20, R, NH, 0.01, 77,
+                                               first_frame_id=100)
+    torch.cuda.synchronize()
+    assert torch.equal(planes_h.raw, planes_d.raw.cpu())
+    assert torch.equal(depth_out, d_dev.cpu()) and torch.equal(normals_out, n_dev.cpu())
+    # f32 / int32 host formats, one chunk
+    planes_f = pm.process_frames_host(dm.cpu().contiguous(), lab.contiguous(), K, 0.15, 0.03, 20, R, NH, 0.01, 77,
+                                      first_frame_id=100, chunk_frames=8)
+    assert torch.equal(planes_f.raw, planes_d.raw.cpu())
+    # and against the oracle for one frame
+    ref = oracle.ransac(d_dev[3].cpu().numpy(), lab[3].numpy(), K, R, NH, 0.01, 77, frame_id=103)
+    assert np.array_equal(planes_h.best_hyp[3].numpy(), ref["best_hyp"])
+    assert np.array_equal(planes_h.inliers[3].numpy(), ref["inliers"])
