@@ -215,7 +215,7 @@ PM_API pm_status pm_process_frames(const float* depth_in, const int32_t* region_
 PM_API int32_t pm_pipeline_kernel_launches(int32_t iters, int32_t n_regions) {
     const int T = pm::adf_default_iters_per_pass();
     const int adf = iters <= 0 ? 1 : (iters + T - 1) / T;
-    return adf + (n_regions > 0 ? 4 /* compaction */ + 3 /* ransac */ : 0);
+    return adf + (n_regions > 0 ? 4 /* compaction */ + 5 /* hyp, score, select, refit, finalize */ : 0);
 }
 
 PM_API const char* pm_status_string(pm_status s) {

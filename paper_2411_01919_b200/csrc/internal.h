@@ -34,6 +34,7 @@ struct RansacWorkspace {
     int32_t* counts;      // [B][R][n_hyp_pad] inlier counts (-1 = invalid)
     uint64_t* errq;       // [B][R][n_hyp_pad] fixed-point error sums (select=ERROR / debug)
     Sums* slots;          // [B][n_slots] refit moments per (region, chunk): slot chunk + region
+    int32_t* best;        // [B][R] selected hypothesis (-1: none)
     size_t total_bytes;
 };
 // Carve `base` (nullable: sizing only) into the ransac workspace.

@@ -291,13 +291,29 @@ PM_DEVINL Sums sums_shfl_xor(const Sums& a, int o) {
     return b;
 }
 
+// ℓ14-17 once per region: one warp per (frame, region) -> best[f][r] (-1:
+// none / too few points).  grid = (ceil(R / 8), B).
+__global__ void __launch_bounds__(256)
+ransac_select_kernel(RansacWorkspace ws, RansacArgs a) {
+    const int r = blockIdx.x * 8 + (threadIdx.x >> 5);
+    const size_t f = blockIdx.y;
+    if (r >= ws.R) return;
+    const int R = ws.R, HP = ws.n_hyp_pad;
+    const int32_t* off = ws.region_off + f * (size_t)(R + 1);
+    int best = -1;
+    if (off[r + 1] - off[r] >= 3) {
+        const Best b = warp_select(ws.counts + (f * R + r) * HP, ws.errq + (f * R + r) * HP, ws.n_hyp, a.select);
+        best = b.score == 0ull ? -1 : b.h;
+    }
+    if ((threadIdx.x & 31) == 0) ws.best[f * R + r] = best;
+}
+
 // grid = (ceil(W*H / kRefitChunk), B).  For every region segment of the
-// chunk: select the winner (warp 0), recount its inliers with the same f32
+// chunk: take the winner (ransac_select_kernel), recount its inliers with the same f32
 // arithmetic, accumulate fp64 moments, write slot (chunk + region).
 __global__ void __launch_bounds__(kScoreThreads)
 ransac_refit_kernel(RansacWorkspace ws, RansacArgs a) {
     __shared__ Sums s_part[kScoreThreads / 32];
-    __shared__ int s_best;
     __shared__ int s_r0;
     const size_t f = blockIdx.y;
     const int R = ws.R, HP = ws.n_hyp_pad;
@@ -320,13 +336,8 @@ ransac_refit_kernel(RansacWorkspace ws, RansacArgs a) {
     const float ifx = 1.0f / a.K.fx, ify = 1.0f / a.K.fy;
     for (int r = s_r0; r < R && off[r] < ce; ++r) {
         const int lo = max(cs, off[r]), hi = min(ce, off[r + 1]);
-        if (hi <= lo || off[r + 1] - off[r] < 3) continue;
-        if (w == 0) {
-            const Best b = warp_select(ws.counts + (f * R + r) * HP, ws.errq + (f * R + r) * HP, ws.n_hyp, a.select);
-            if (lane == 0) s_best = b.score == 0ull ? -1 : b.h;
-        }
-        __syncthreads();
-        const int best = s_best;
+        if (hi <= lo) continue;
+        const int best = ws.best[f * R + r];
         if (best >= 0) {
             const float4 pl = ws.planes[(f * R + r) * HP + best];
             const uint2 q0 = pts[off[r]];
@@ -433,10 +444,8 @@ ransac_finalize_kernel(RansacWorkspace ws, RansacArgs a, pm_plane* __restrict__ 
     res.d = 0.f; res.inliers = 0; res.n_points = n; res.best_hyp = -1; res.sum_dist = 0.f;
     pm_plane* out = planes_out + f * R + r;
     if (n < 3) { res.status = PM_PLANE_TOO_FEW; *out = res; return; }
-    Best b{0ull, 0x7FFFFFFF};
-    for (int h = 0; h < NH; ++h) best_merge(b, hyp_score(a.select, counts[h], errq[h]), h);
-    if (b.score == 0ull) { res.status = PM_PLANE_DEGENERATE; *out = res; return; }
-    const int best = b.h;
+    const int best = ws.best[f * R + r];
+    if (best < 0) { res.status = PM_PLANE_DEGENERATE; *out = res; return; }
     const float4 pl = ws.planes[(f * R + r) * HP + best];
     // slots of this region: chunks c0..c1 -> slot c + r (ascending order)
     const int c0 = base / kRefitChunk, c1 = (base + n - 1) / kRefitChunk;
@@ -524,6 +533,7 @@ RansacWorkspace ransac_workspace_layout(void* base, int W, int H, int R, int n_h
     ws.counts = (int32_t*)take(sizeof(int32_t) * B * Rm * ws.n_hyp_pad);
     ws.errq = (uint64_t*)take(sizeof(uint64_t) * B * Rm * ws.n_hyp_pad);
     ws.slots = (Sums*)take(sizeof(Sums) * B * (size_t)ws.n_slots);
+    ws.best = (int32_t*)take(sizeof(int32_t) * B * Rm);
     ws.total_bytes = o;
     return ws;
 }
@@ -553,6 +563,7 @@ cudaError_t ransac_run(const RansacWorkspace& ws, const RansacArgs& a, pm_plane*
 #undef PM_SCORE
     if (!launched) return cudaErrorInvalidConfiguration;
     const dim3 g_refit((unsigned)(((size_t)ws.W * ws.H + kRefitChunk - 1) / kRefitChunk), ws.B);
+    ransac_select_kernel<<<dim3((ws.R + 7) / 8, ws.B), 256, 0, stream>>>(ws, a);
     ransac_refit_kernel<<<g_refit, kScoreThreads, 0, stream>>>(ws, a);
     ransac_finalize_kernel<<<dim3((ws.R + kFinalThreads - 1) / kFinalThreads, ws.B), kFinalThreads, 0, stream>>>(
         ws, a, planes);
