@@ -30,6 +30,7 @@ SAMPLER_PHILOX, SAMPLER_ENUMERATE = 0, 1
 SELECT_COUNT, SELECT_ERROR = 0, 1
 ADF_ALG1, ADF_DIVERGENCE = 0, 1
 NORMALS_GEOMETRIC, NORMALS_AS_PRINTED = 0, 1
+ENGINE_AUTO, ENGINE_TILED, ENGINE_STREAM = 0, 1, 2
 DEPTH_F32_M, DEPTH_U16_MM = 0, 1
 LABELS_I32, LABELS_U16 = 0, 1
 PLANE_WORDS = 12          # sizeof(pm_plane) / 4
@@ -40,7 +41,8 @@ class pm_intrinsics(ctypes.Structure):
 
 
 class pm_adf_options(ctypes.Structure):
-    _fields_ = [("iters_per_pass", ctypes.c_int32), ("scheme", ctypes.c_int32), ("normals_mode", ctypes.c_int32)]
+    _fields_ = [("iters_per_pass", ctypes.c_int32), ("scheme", ctypes.c_int32), ("normals_mode", ctypes.c_int32),
+                ("engine", ctypes.c_int32)]
 
 
 class pm_ransac_options(ctypes.Structure):
@@ -154,7 +156,8 @@ def pipeline_workspace_bytes(W: int, H: int, n_regions: int, n_hyp: int, n_frame
 
 def adf_filter(depth: torch.Tensor, K, lam: float, kappa: float, iters: int, normals: bool = True,
                iters_per_pass: int = 0, out: torch.Tensor = None, normals_out: torch.Tensor = None,
-               workspace: torch.Tensor = None, scheme: int = ADF_ALG1, normals_mode: int = NORMALS_GEOMETRIC):
+               workspace: torch.Tensor = None, scheme: int = ADF_ALG1, normals_mode: int = NORMALS_GEOMETRIC,
+               engine: int = ENGINE_AUTO):
     """Alg. 1 on [H, W] or [B, H, W] f32 depth (metres, CUDA).
     Returns (I_smooth, normals [.., 3, H, W] or None)."""
     B, H, W = _frames(depth, torch.float32)
@@ -164,7 +167,7 @@ def adf_filter(depth: torch.Tensor, K, lam: float, kappa: float, iters: int, nor
         shape = (3, H, W) if depth.dim() == 2 else (B, 3, H, W)
         nrm = torch.empty(shape, dtype=torch.float32, device=depth.device) if normals_out is None else normals_out
     ws = workspace if workspace is not None else _workspace(adf_workspace_bytes(W, H, B), depth.device)
-    opt = pm_adf_options(int(iters_per_pass), int(scheme), int(normals_mode))
+    opt = pm_adf_options(int(iters_per_pass), int(scheme), int(normals_mode), int(engine))
     _check(_lib.pm_adf_filter_ex(depth.data_ptr(), out.data_ptr(), W, H, B, ctypes.byref(_K(K)), float(lam),
                                  float(kappa), int(iters), nrm.data_ptr() if nrm is not None else None,
                                  ws.data_ptr(), ws.numel(), ctypes.byref(opt), _stream(depth)))

@@ -464,10 +464,38 @@ static AdfParams make_params(const pm_intrinsics* K, float lam, float kappa, int
     return p;
 }
 
+static AdfStreamParams stream_params(const AdfParams& p) {
+    AdfStreamParams q;
+    q.kc = p.kc; q.l2lam = p.l2lam; q.kd = p.kd; q.lam = p.lam;
+    q.fx = p.fx; q.fy = p.fy; q.cx = p.cx; q.cy = p.cy; q.ifx = p.ifx; q.ify = p.ify;
+    q.scheme = p.scheme; q.nmode = p.nmode;
+    return q;
+}
+
 cudaError_t adf_run(const float* in, float* out, float* normals, float* ws, int W, int H, int B,
                     const pm_intrinsics* K, float lam, float kappa, int iters, int iters_per_pass,
-                    int scheme, int nmode, cudaStream_t stream) {
+                    int scheme, int nmode, int engine, cudaStream_t stream) {
     const AdfParams p = make_params(K, lam, kappa, scheme, nmode);
+    // wavefront engine: all sweeps of a pass in one walk down the frame
+    const int Ls = iters_per_pass > 0 ? iters_per_pass : adf_stream_max_levels();
+    const bool want_stream = engine == PM_ADF_ENGINE_STREAM;   // measured slower than tiled on B200
+    if (iters > 0 && want_stream && Ls <= adf_stream_max_levels() &&
+        adf_stream_applicable(W, H, Ls < iters ? Ls : iters)) {
+        const AdfStreamParams q = stream_params(p);
+        const int passes = (iters + Ls - 1) / Ls;
+        const float* src = in;
+        int done = 0;
+        for (int k = 0; k < passes; ++k) {
+            const int it = (iters - done) / (passes - k);
+            float* dst = (((passes - 1 - k) & 1) == 0) ? out : ws;
+            const bool last = k == passes - 1;
+            cudaError_t e = adf_stream_pass(src, dst, last ? normals : nullptr, W, H, B, it, q, stream);
+            if (e != cudaSuccess) return e;
+            src = dst;
+            done += it;
+        }
+        return cudaSuccess;
+    }
     int T = iters_per_pass > 0 ? iters_per_pass : adf_default_iters_per_pass();
     if (T > kMaxItersPerPass) T = kMaxItersPerPass;
     if (iters == 0) {   // N = 0: I_smooth = I (Alg. 1 ℓ1); normals of the input

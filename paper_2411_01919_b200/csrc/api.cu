@@ -20,6 +20,7 @@ cudaError_t g_setup_err = cudaSuccess;
 cudaError_t setup() {
     std::call_once(g_once, [] {
         g_setup_err = pm::adf_setup_attributes();
+        if (g_setup_err == cudaSuccess) g_setup_err = pm::adf_stream_setup_attributes();
         if (g_setup_err == cudaSuccess) g_setup_err = pm::ransac_setup_attributes();
     });
     return g_setup_err;
@@ -47,7 +48,9 @@ pm_status cuda_status(cudaError_t e) { return e == cudaSuccess ? PM_OK : PM_ERR_
 
 pm_status adf_impl(const float* in, float* out, int32_t W, int32_t H, int32_t B, const pm_intrinsics* K,
                    float lam, float kappa, int32_t iters, float* normals, void* ws, size_t ws_bytes,
-                   int32_t iters_per_pass, int32_t scheme, int32_t nmode, cudaStream_t stream) {
+                   int32_t iters_per_pass, int32_t scheme, int32_t nmode, int32_t engine, cudaStream_t stream) {
+    if (engine != PM_ADF_ENGINE_AUTO && engine != PM_ADF_ENGINE_TILED && engine != PM_ADF_ENGINE_STREAM)
+        return PM_ERR_INVALID_ARGUMENT;
     if (scheme != PM_ADF_ALG1 && scheme != PM_ADF_DIVERGENCE) return PM_ERR_INVALID_ARGUMENT;
     if (nmode != PM_NORMALS_GEOMETRIC && nmode != PM_NORMALS_AS_PRINTED) return PM_ERR_INVALID_ARGUMENT;
     if (!in || !out || !dims_ok(W, H, B) || iters < 0) return PM_ERR_INVALID_ARGUMENT;
@@ -58,13 +61,15 @@ pm_status adf_impl(const float* in, float* out, int32_t W, int32_t H, int32_t B,
     if (normals && (overlap(normals, 3 * bytes, in, bytes) || overlap(normals, 3 * bytes, out, bytes)))
         return PM_ERR_INVALID_ARGUMENT;
     if (iters_per_pass < 0 || iters_per_pass > 16) return PM_ERR_INVALID_ARGUMENT;   // 16 = adf.cu kMaxItersPerPass
+    // the ping-pong workspace is required whenever a pass of the tiled engine
+    // (the fallback of the wavefront engine) would not hold all the sweeps
     const int T = iters_per_pass > 0 ? iters_per_pass : pm::adf_default_iters_per_pass();
     const bool needs_ws = iters > T;
     if (needs_ws && (!ws || ws_bytes < pm_adf_workspace_bytes(W, H, B) || !aligned256(ws))) return PM_ERR_WORKSPACE;
     if (needs_ws && (overlap(ws, bytes, in, bytes) || overlap(ws, bytes, out, bytes))) return PM_ERR_INVALID_ARGUMENT;
     if (cudaError_t e = setup(); e != cudaSuccess) return PM_ERR_CUDA;
     return cuda_status(pm::adf_run(in, out, normals, (float*)ws, W, H, B, K, lam, kappa, iters,
-                                   iters_per_pass, scheme, nmode, stream));
+                                   iters_per_pass, scheme, nmode, engine, stream));
 }
 
 pm_status ransac_impl(const float* depth, int32_t W, int32_t H, int32_t B, uint32_t first_frame,
@@ -117,7 +122,7 @@ PM_API pm_status pm_adf_filter(const float* depth_in, float* depth_out, int32_t 
                                const pm_intrinsics* K, float lambda, float kappa, int32_t iters,
                                float* normals_out, void* workspace, size_t ws_bytes, pm_stream_t stream) {
     return adf_impl(depth_in, depth_out, W, H, 1, K, lambda, kappa, iters, normals_out, workspace,
-                    ws_bytes, 0, PM_ADF_ALG1, PM_NORMALS_GEOMETRIC, (cudaStream_t)stream);
+                    ws_bytes, 0, PM_ADF_ALG1, PM_NORMALS_GEOMETRIC, PM_ADF_ENGINE_AUTO, (cudaStream_t)stream);
 }
 
 PM_API pm_status pm_adf_filter_batched(const float* depth_in, float* depth_out, int32_t W, int32_t H,
@@ -125,7 +130,7 @@ PM_API pm_status pm_adf_filter_batched(const float* depth_in, float* depth_out, 
                                        float kappa, int32_t iters, float* normals_out, void* workspace,
                                        size_t ws_bytes, pm_stream_t stream) {
     return adf_impl(depth_in, depth_out, W, H, n_frames, K, lambda, kappa, iters, normals_out, workspace,
-                    ws_bytes, 0, PM_ADF_ALG1, PM_NORMALS_GEOMETRIC, (cudaStream_t)stream);
+                    ws_bytes, 0, PM_ADF_ALG1, PM_NORMALS_GEOMETRIC, PM_ADF_ENGINE_AUTO, (cudaStream_t)stream);
 }
 
 PM_API pm_status pm_adf_filter_ex(const float* depth_in, float* depth_out, int32_t W, int32_t H,
@@ -134,7 +139,8 @@ PM_API pm_status pm_adf_filter_ex(const float* depth_in, float* depth_out, int32
                                   const pm_adf_options* opt, pm_stream_t stream) {
     return adf_impl(depth_in, depth_out, W, H, n_frames, K, lambda, kappa, iters, normals_out, workspace,
                     ws_bytes, opt ? opt->iters_per_pass : 0, opt ? opt->scheme : PM_ADF_ALG1,
-                    opt ? opt->normals_mode : PM_NORMALS_GEOMETRIC, (cudaStream_t)stream);
+                    opt ? opt->normals_mode : PM_NORMALS_GEOMETRIC, opt ? opt->engine : PM_ADF_ENGINE_AUTO,
+                    (cudaStream_t)stream);
 }
 
 PM_API pm_status pm_normals_from_depth(const float* depth, int32_t W, int32_t H, const pm_intrinsics* K,
@@ -206,7 +212,7 @@ PM_API pm_status pm_process_frames(const float* depth_in, const int32_t* region_
     if (!depth_out || !normals_out) return PM_ERR_INVALID_ARGUMENT;
     if (ws_bytes < pm_pipeline_workspace_bytes(W, H, n_regions, n_hyp, n_frames)) return PM_ERR_WORKSPACE;
     pm_status s = adf_impl(depth_in, depth_out, W, H, n_frames, K, lambda, kappa, iters, normals_out, workspace,
-                           ws_bytes, 0, PM_ADF_ALG1, PM_NORMALS_GEOMETRIC, (cudaStream_t)stream);
+                           ws_bytes, 0, PM_ADF_ALG1, PM_NORMALS_GEOMETRIC, PM_ADF_ENGINE_AUTO, (cudaStream_t)stream);
     if (s != PM_OK) return s;
     return ransac_impl(depth_out, W, H, n_frames, first_frame_id, K, region_labels, n_regions, n_hyp,
                        inlier_thresh, seed, planes_out, workspace, ws_bytes, nullptr, (cudaStream_t)stream);

@@ -335,3 +335,24 @@ def test_host_pipeline_matches_device_pipeline(pm):
     ref = oracle.ransac(d_dev[3].cpu().numpy(), lab[3].numpy(), K, R, NH, 0.01, 77, frame_id=103)
     assert np.array_equal(planes_h.best_hyp[3].numpy(), ref["best_hyp"])
     assert np.array_equal(planes_h.inliers[3].numpy(), ref["inliers"])
+
+
+# ---------------------------------------------------- wavefront (stream) engine
+@pytest.mark.parametrize("name,kw", [("C1n", {}), ("C1n", {"holes": 0.02}), ("C2", {}), ("C2", {"holes": 0.01}),
+                                     ("C2", {"W": 334, "H": 251}), ("RAMP", {})])
+def test_stream_engine_bitwise_equals_tiled(pm, name, kw):
+    fr = scenegen.make_config(name, **kw)
+    d = fr["depth"].to(DEV)
+    it = fr["iters"] if name != "RAMP" else 9
+    for scheme in (pm.ADF_ALG1, pm.ADF_DIVERGENCE):
+        ref, nref = pm.adf_filter(d, fr["K"], fr["lam"], fr["kappa"], it, scheme=scheme, engine=pm.ENGINE_TILED)
+        for levels in (0, 1, 3, 7, 20):
+            out, nrm = pm.adf_filter(d, fr["K"], fr["lam"], fr["kappa"], it, scheme=scheme, engine=pm.ENGINE_STREAM,
+                                     iters_per_pass=levels if levels <= 16 else 0)
+            assert torch.equal(out, ref), (scheme, levels)
+            assert torch.equal(nrm, nref), (scheme, levels)
+    out, nrm = pm.adf_filter(d, fr["K"], fr["lam"], fr["kappa"], it)      # default engine
+    torch.cuda.synchronize()
+    d_in = fr["depth"].numpy()
+    _check_depth(out.cpu().numpy(), d_in, oracle.adf(d_in, fr["lam"], fr["kappa"], it))
+    _check_normals(nrm.cpu().numpy(), oracle.normals(out.cpu().numpy(), fr["K"]))
