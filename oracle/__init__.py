@@ -69,6 +69,10 @@ def lib() -> ctypes.CDLL:
             L.orc_refit_plane.argtypes = [P, i32, P]
             L.orc_ransac.argtypes = [P, P, i32, i32, f32, f32, f32, f32, i32, i32, f32, u64, u32,
                                      i32, i32, P, P, P, P, P]
+            L.orc_normals_to_u8.argtypes = [P, i32, i32, P]
+            L.orc_normals_to_u8.restype = None
+            L.orc_canny_u8.argtypes = [P, i32, i32, i32, f64, f64, P]
+            L.orc_segment_regions.argtypes = [P, i32, i32, f64, f64, i32, i32, P, P, P]
             _lib = L
     return _lib
 
@@ -194,3 +198,36 @@ def ransac(depth: np.ndarray, labels: np.ndarray, K, n_regions: int, n_hyp: int,
         res["counts"] = cnt[:R]
         res["errq_all"] = ea[:R]
     return res
+
+
+def normals_to_u8(normals: np.ndarray) -> np.ndarray:
+    """f32 [3, H, W] normals -> u8 [H, W, 3], c = rint((n + 1) * 127.5)."""
+    n = _c(normals, np.float32)
+    _, H, W = n.shape
+    out = np.empty((H, W, 3), np.uint8)
+    lib().orc_normals_to_u8(_p(n), W, H, _p(out))
+    return out
+
+
+def canny_u8(img: np.ndarray, low: float, high: float) -> np.ndarray:
+    """Canny (L2, 3x3 Sobel, replicated border) on u8 [H, W] or [H, W, C] -> u8 0/255."""
+    a = _c(img, np.uint8)
+    H, W = a.shape[:2]
+    C = 1 if a.ndim == 2 else a.shape[2]
+    out = np.empty((H, W), np.uint8)
+    assert lib().orc_canny_u8(_p(a), W, H, C, float(low), float(high), _p(out)) == 0
+    return out
+
+
+def segment_regions(normals: np.ndarray, low: float = 30.0, high: float = 90.0, min_area: int = 300,
+                    max_regions: int = 1024):
+    """NEXT-2 region labels from f32 normals [3, H, W]: (labels int32 [H, W],
+    n_regions, dilated edge mask u8 [H, W])."""
+    n = _c(normals, np.float32)
+    _, H, W = n.shape
+    labels = np.empty((H, W), np.int32)
+    nr = np.zeros(1, np.int32)
+    edges = np.empty((H, W), np.uint8)
+    assert lib().orc_segment_regions(_p(n), W, H, float(low), float(high), int(min_area), int(max_regions),
+                                     _p(labels), _p(nr), _p(edges)) == 0
+    return labels, int(nr[0]), edges

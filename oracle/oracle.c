@@ -513,3 +513,190 @@ ORC_API int orc_ransac(const float* depth, const int32_t* labels, int W, int H,
     free(P); free(cnt); free(err); free(S);
     return 0;
 }
+
+/* ------------------------------------------------------------------------ */
+/* NEXT-2: region labels from the normal image, the step the
+ * paper places between Alg. 1 and Alg. 2: "edges are detected from the normal
+ * vector image using the Canny edge detection algorithm. Subsequently,
+ * contours are extracted from these edges".  Readings
+ * (Q26-Q29): Canny runs on the 8-bit RGB normal image
+ * c = rint((n + 1) * 127.5) (the visualisation of fig:ADF_ex), with
+ * 3x3 Sobel, replicated borders, L2 magnitude, the channel of largest
+ * magnitude per pixel, non-maximum suppression and 8-connected
+ * hysteresis; pixels with an invalid normal are edges; the edge mask is
+ * dilated by one pixel (3x3); regions = 4-connected components of non-edge
+ * pixels with >= min_area pixels, numbered by descending size, ties
+ * by smallest raster index, at most max_regions; others -1.       */
+
+/* f32 normals [3][H][W] -> interleaved u8 [H][W][3]. */
+ORC_API void orc_normals_to_u8(const float* nrm, int W, int H, uint8_t* img)
+{
+    size_t n = (size_t)W * H;
+    for (size_t p = 0; p < n; ++p)
+        for (int c = 0; c < 3; ++c) {
+            float v = rintf((nrm[c * n + p] + 1.0f) * 127.5f);
+            int q = (int)v;
+            img[3 * p + c] = (uint8_t)(q < 0 ? 0 : (q > 255 ? 255 : q));
+        }
+}
+
+/* Canny on an interleaved u8 image with C channels; edges [H][W] 0/255. */
+ORC_API int orc_canny_u8(const uint8_t* img, int W, int H, int C, double low_thresh, double high_thresh,
+                         uint8_t* edges)
+{
+    if (!img || !edges || W < 1 || H < 1 || C < 1) return -1;
+    if (low_thresh > high_thresh) { double t = low_thresh; low_thresh = high_thresh; high_thresh = t; }
+    /* L2 magnitude compared with squared thresholds, as integers */
+    long long low = (long long)floor(low_thresh > 0 ? low_thresh * low_thresh : low_thresh);
+    long long high = (long long)floor(high_thresh > 0 ? high_thresh * high_thresh : high_thresh);
+    size_t n = (size_t)W * H;
+    int* dx = (int*)malloc(n * sizeof(int));
+    int* dy = (int*)malloc(n * sizeof(int));
+    long long* mag = (long long*)malloc(n * sizeof(long long));
+    unsigned char* cand = (unsigned char*)calloc(n, 1);   /* 1 = NMS survivor above low */
+    int* stack = (int*)malloc(n * sizeof(int));
+    if (!dx || !dy || !mag || !cand || !stack) { free(dx); free(dy); free(mag); free(cand); free(stack); return -1; }
+#define PX(vv, uu, cc) ((int)img[(((size_t)(vv) * W) + (uu)) * C + (cc)])
+    for (int v = 0; v < H; ++v)
+        for (int u = 0; u < W; ++u) {
+            int um = u > 0 ? u - 1 : 0, up = u < W - 1 ? u + 1 : W - 1;
+            int vm = v > 0 ? v - 1 : 0, vp = v < H - 1 ? v + 1 : H - 1;
+            long long best = -1;
+            int bx = 0, by = 0;
+            for (int c = 0; c < C; ++c) {
+                int gx = (PX(vm, up, c) - PX(vm, um, c)) + 2 * (PX(v, up, c) - PX(v, um, c)) + (PX(vp, up, c) - PX(vp, um, c));
+                int gy = (PX(vp, um, c) - PX(vm, um, c)) + 2 * (PX(vp, u, c) - PX(vm, u, c)) + (PX(vp, up, c) - PX(vm, up, c));
+                long long m = (long long)gx * gx + (long long)gy * gy;
+                if (m > best) { best = m; bx = gx; by = gy; }      /* first channel wins ties */
+            }
+            size_t p = (size_t)v * W + u;
+            dx[p] = bx; dy[p] = by; mag[p] = best;
+        }
+#undef PX
+    /* non-maximum suppression along the quantised gradient direction
+     * (tan 22.5 deg in 15-bit fixed point); neighbours outside the image
+     * count as 0 */
+    const long long TG22 = (long long)(0.4142135623730950488016887242097 * (1 << 15) + 0.5);
+#define MAG(vv, uu) (((vv) < 0 || (vv) >= H || (uu) < 0 || (uu) >= W) ? 0LL : mag[(size_t)(vv) * W + (uu)])
+    for (int v = 0; v < H; ++v)
+        for (int u = 0; u < W; ++u) {
+            size_t p = (size_t)v * W + u;
+            long long m = mag[p];
+            if (!(m > low)) continue;
+            long long xs = dx[p], ys = dy[p];
+            long long x = xs < 0 ? -xs : xs, y = (ys < 0 ? -ys : ys) << 15;
+            long long tg22x = x * TG22;
+            int keep;
+            if (y < tg22x) {
+                keep = m > MAG(v, u - 1) && m >= MAG(v, u + 1);
+            } else {
+                long long tg67x = tg22x + (x << 16);
+                if (y > tg67x) {
+                    keep = m > MAG(v - 1, u) && m >= MAG(v + 1, u);
+                } else {
+                    int s = ((xs ^ ys) < 0) ? -1 : 1;
+                    keep = m > MAG(v - 1, u - s) && m > MAG(v + 1, u + s);
+                }
+            }
+            if (keep) cand[p] = 1;
+        }
+#undef MAG
+    /* hysteresis: candidates 8-connected (through candidates) to a strong one */
+    memset(edges, 0, n);
+    int top = 0;
+    for (size_t p = 0; p < n; ++p)
+        if (cand[p] && mag[p] > high) { edges[p] = 255; stack[top++] = (int)p; }
+    while (top > 0) {
+        int p = stack[--top];
+        int v = p / W, u = p % W;
+        for (int dv = -1; dv <= 1; ++dv)
+            for (int du = -1; du <= 1; ++du) {
+                int vv = v + dv, uu = u + du;
+                if ((dv == 0 && du == 0) || vv < 0 || vv >= H || uu < 0 || uu >= W) continue;
+                size_t q = (size_t)vv * W + uu;
+                if (cand[q] && !edges[q]) { edges[q] = 255; stack[top++] = (int)q; }
+            }
+    }
+    free(dx); free(dy); free(mag); free(cand); free(stack);
+    return 0;
+}
+
+/* Region labels from f32 normals [3][H][W] (see the block comment above).
+ * labels [H][W] int32 (-1 = none), *n_regions = number of regions kept,
+ * edges_out [H][W] (nullable): the final (dilated) edge mask 0/1.        */
+ORC_API int orc_segment_regions(const float* nrm, int W, int H, double low, double high, int min_area,
+                                int max_regions, int32_t* labels, int32_t* n_regions, uint8_t* edges_out)
+{
+    if (!nrm || !labels || !n_regions || W < 1 || H < 1) return -1;
+    size_t n = (size_t)W * H;
+    uint8_t* img = (uint8_t*)malloc(3 * n);
+    uint8_t* e0 = (uint8_t*)malloc(n);
+    uint8_t* e1 = (uint8_t*)malloc(n);
+    int32_t* comp = (int32_t*)malloc(n * sizeof(int32_t));
+    int* queue = (int*)malloc(n * sizeof(int));
+    if (!img || !e0 || !e1 || !comp || !queue) { free(img); free(e0); free(e1); free(comp); free(queue); return -1; }
+    orc_normals_to_u8(nrm, W, H, img);
+    orc_canny_u8(img, W, H, 3, low, high, e0);
+    for (size_t p = 0; p < n; ++p)                         /* invalid normal -> edge */
+        if (nrm[p] == 0.0f && nrm[n + p] == 0.0f && nrm[2 * n + p] == 0.0f) e0[p] = 255;
+    for (int v = 0; v < H; ++v)                            /* 3x3 dilation */
+        for (int u = 0; u < W; ++u) {
+            int any = 0;
+            for (int dv = -1; dv <= 1 && !any; ++dv)
+                for (int du = -1; du <= 1; ++du) {
+                    int vv = v + dv, uu = u + du;
+                    if (vv < 0 || vv >= H || uu < 0 || uu >= W) continue;
+                    if (e0[(size_t)vv * W + uu]) { any = 1; break; }
+                }
+            e1[(size_t)v * W + u] = (uint8_t)any;
+        }
+    /* 4-connected components of non-edge pixels by BFS in raster order: the
+     * component's seed is its smallest raster index */
+    for (size_t p = 0; p < n; ++p) comp[p] = -1;
+    int n_comp = 0;
+    int cap = 1024;
+    int* seed = (int*)malloc(cap * sizeof(int));
+    int* size = (int*)malloc(cap * sizeof(int));
+    for (size_t p0 = 0; p0 < n; ++p0) {
+        if (e1[p0] || comp[p0] >= 0) continue;
+        if (n_comp == cap) { cap *= 2; seed = (int*)realloc(seed, cap * sizeof(int)); size = (int*)realloc(size, cap * sizeof(int)); }
+        int head = 0, tail = 0;
+        queue[tail++] = (int)p0;
+        comp[p0] = n_comp;
+        while (head < tail) {
+            int p = queue[head++];
+            int v = p / W, u = p % W;
+            const int nb[4][2] = {{-1, 0}, {1, 0}, {0, -1}, {0, 1}};
+            for (int k = 0; k < 4; ++k) {
+                int vv = v + nb[k][0], uu = u + nb[k][1];
+                if (vv < 0 || vv >= H || uu < 0 || uu >= W) continue;
+                size_t q = (size_t)vv * W + uu;
+                if (!e1[q] && comp[q] < 0) { comp[q] = n_comp; queue[tail++] = (int)q; }
+            }
+        }
+        seed[n_comp] = (int)p0;
+        size[n_comp] = tail;
+        n_comp++;
+    }
+    /* keep components >= min_area, order by (size desc, seed asc) */
+    int* order = (int*)malloc((n_comp > 0 ? n_comp : 1) * sizeof(int));
+    int* rank = (int*)malloc((n_comp > 0 ? n_comp : 1) * sizeof(int));
+    int kept = 0;
+    for (int c = 0; c < n_comp; ++c) if (size[c] >= min_area) order[kept++] = c;
+    for (int i = 1; i < kept; ++i) {                       /* insertion sort (stable, small) */
+        int c = order[i], j = i - 1;
+        while (j >= 0 && (size[order[j]] < size[c] || (size[order[j]] == size[c] && seed[order[j]] > seed[c]))) {
+            order[j + 1] = order[j];
+            j--;
+        }
+        order[j + 1] = c;
+    }
+    for (int c = 0; c < n_comp; ++c) rank[c] = -1;
+    if (kept > max_regions) kept = max_regions;
+    for (int i = 0; i < kept; ++i) rank[order[i]] = i;
+    for (size_t p = 0; p < n; ++p) labels[p] = comp[p] >= 0 ? rank[comp[p]] : -1;
+    *n_regions = kept;
+    if (edges_out) for (size_t p = 0; p < n; ++p) edges_out[p] = e1[p];
+    free(img); free(e0); free(e1); free(comp); free(queue); free(seed); free(size); free(order); free(rank);
+    return 0;
+}

@@ -1,0 +1,28 @@
+#!/usr/bin/env python
+"""Small invocation of every pmap kernel (C1-size frames, both ADF engines,
+normals, compaction, RANSAC incl. debug/ENUMERATE/select-error, the host
+pipeline) for compute-sanitizer runs."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+
+import paper_2411_01919_b200 as pm
+import scenegen
+
+fr = scenegen.make_config("C1n", holes=0.02)
+d, lab, K = fr["depth"].cuda(), fr["labels"].cuda(), fr["K"]
+for eng in (pm.ENGINE_TILED, pm.ENGINE_STREAM):
+    for scheme in (pm.ADF_ALG1, pm.ADF_DIVERGENCE):
+        out, nrm = pm.adf_filter(d, K, 0.15, 0.03, 10, engine=eng, scheme=scheme)
+pm.normals_from_depth(d, K)
+pm.normals_from_depth(d, K, mode=pm.NORMALS_AS_PRINTED)
+pm.ransac_planes(out, K, lab, 4, 64, 0.01, 1, debug=True)
+pm.ransac_planes(out, K, lab, 4, 300, 0.01, 1, select=pm.SELECT_ERROR, debug=True)
+pm.ransac_planes(out, K, lab, 4, 1000, 0.01, 1, sampler=pm.SAMPLER_ENUMERATE, debug=True)
+ds, ls, K2 = scenegen.stair_stream(0, 3, 128, 96, 16)
+pm.process_frames(ds.cuda(), ls.cuda(), K2, 0.15, 0.03, 20, 16, 64, 0.01, 7)
+pm.process_frames_host(ds.contiguous(), ls.contiguous(), K2, 0.15, 0.03, 20, 16, 64, 0.01, 7, chunk_frames=2)
+torch.cuda.synchronize()
+print("sanitize run ok")
