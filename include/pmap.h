@@ -221,6 +221,37 @@ PM_API size_t pm_pipeline_workspace_bytes(int32_t W, int32_t H, int32_t n_region
                                           int32_t n_frames);
 
 /* ---------------------------------------------------------------------- */
+/* segment_regions — NEXT-2 of SURVEY §8(f): region labels from the normal
+ * image, the paper's step between Alg. 1 and Alg. 2 ("edges are detected from
+ * the normal vector image using the Canny edge detection algorithm.
+ * Subsequently, contours are extracted from these edges").
+ * Readings (Q26-Q29): Canny on the 8-bit RGB normal image
+ * c = rint((n + 1) * 127.5) with 3x3 Sobel, replicated borders, the
+ * L2 magnitude of the strongest channel, non-maximum suppression and
+ * 8-connected hysteresis (canny_low / canny_high on that magnitude, as
+ * OpenCV's Canny with L2gradient); pixels with an invalid normal are edges;
+ * the edge mask is dilated by one pixel (3x3); regions are the 4-connected
+ * components of non-edge pixels with >= min_area pixels, numbered
+ * 0.. by descending size, ties by smallest raster index, at most
+ * max_regions; all other pixels -1.  Integer decisions only: bit-exact.
+ *   normals      [B][3][H][W] f32 (from adf_filter / normals_from_depth)
+ *   labels_out   [B][H][W] int32
+ *   n_regions_out [B] int32 (device, nullable): regions kept per frame
+ *   edges_out    [B][H][W] uint8 0/1 (device, nullable): the dilated edge mask
+ *   workspace    >= pm_segment_workspace_bytes(W, H, n_frames, min_area). */
+typedef struct {
+    float canny_low;          /* default 30 */
+    float canny_high;         /* default 90         */
+    int32_t min_area;         /* default 300 px     */
+    int32_t max_regions;      /* <= 65536           */
+} pm_segment_params;
+PM_API pm_status pm_segment_regions(const float* normals, int32_t W, int32_t H, int32_t n_frames,
+                                    const pm_segment_params* params, int32_t* labels_out,
+                                    int32_t* n_regions_out, uint8_t* edges_out, void* workspace,
+                                    size_t ws_bytes, pm_stream_t stream);
+PM_API size_t pm_segment_workspace_bytes(int32_t W, int32_t H, int32_t n_frames, int32_t min_area);
+
+/* ---------------------------------------------------------------------- */
 /* The whole path for frames in HOST memory: chunks of chunk_frames frames
  * are copied to the device, processed by pm_process_frames and the plane
  * tables (and, if the pointers are not NULL, the filtered depth [B][H][W] and

@@ -45,6 +45,11 @@ class pm_adf_options(ctypes.Structure):
                 ("engine", ctypes.c_int32)]
 
 
+class pm_segment_params(ctypes.Structure):
+    _fields_ = [("canny_low", ctypes.c_float), ("canny_high", ctypes.c_float), ("min_area", ctypes.c_int32),
+                ("max_regions", ctypes.c_int32)]
+
+
 class pm_ransac_options(ctypes.Structure):
     _fields_ = [("sampler", ctypes.c_int32), ("select", ctypes.c_int32),
                 ("counts_out", ctypes.c_void_p), ("errq_out", ctypes.c_void_p)]
@@ -83,10 +88,13 @@ _lib.pm_process_frames_host.argtypes = [_P, _I32, _P, _I32, _I32, _I32, _I32, _U
 _lib.pm_host_pipeline_arena_bytes.restype = _SZ
 _lib.pm_host_pipeline_arena_bytes.argtypes = [_I32, _I32, _I32, _I32, _I32, _I32, _I32]
 _lib.pm_depth_u16_to_metres.argtypes = [_P, _P, _SZ, _F32, _P]
+_lib.pm_segment_regions.argtypes = [_P, _I32, _I32, _I32, ctypes.POINTER(pm_segment_params), _P, _P, _P, _P, _SZ, _P]
+_lib.pm_segment_workspace_bytes.restype = _SZ
+_lib.pm_segment_workspace_bytes.argtypes = [_I32, _I32, _I32, _I32]
 for _fn in ("pm_adf_filter", "pm_adf_filter_batched", "pm_adf_filter_ex", "pm_normals_from_depth",
             "pm_normals_from_depth_batched", "pm_normals_from_depth_ex", "pm_ransac_planes",
             "pm_ransac_planes_batched", "pm_ransac_planes_ex", "pm_process_frames", "pm_process_frames_host",
-            "pm_depth_u16_to_metres"):
+            "pm_depth_u16_to_metres", "pm_segment_regions"):
     getattr(_lib, _fn).restype = ctypes.c_int
 
 EXPORTED = ("pm_adf_filter", "pm_adf_filter_batched", "pm_adf_filter_ex", "pm_adf_workspace_bytes",
@@ -94,6 +102,7 @@ EXPORTED = ("pm_adf_filter", "pm_adf_filter_batched", "pm_adf_filter_ex", "pm_ad
             "pm_ransac_planes_batched", "pm_ransac_planes_ex", "pm_ransac_workspace_bytes",
             "pm_process_frames", "pm_pipeline_workspace_bytes", "pm_pipeline_kernel_launches",
             "pm_process_frames_host", "pm_host_pipeline_arena_bytes", "pm_depth_u16_to_metres",
+            "pm_segment_regions", "pm_segment_workspace_bytes",
             "pm_status_string", "pm_version")
 
 
@@ -319,3 +328,33 @@ def process_frames_host(depth: torch.Tensor, labels: torch.Tensor, K, lam: float
                                            normals_out.data_ptr() if normals_out is not None else None, C,
                                            arena.data_ptr(), arena.numel(), stream))
     return Planes(planes_out)
+
+
+def segment_workspace_bytes(W: int, H: int, n_frames: int = 1, min_area: int = 300) -> int:
+    return int(_lib.pm_segment_workspace_bytes(W, H, n_frames, min_area))
+
+
+def segment_regions(normals: torch.Tensor, canny_low: float = 30.0, canny_high: float = 90.0, min_area: int = 300,
+                    max_regions: int = 1024, edges: bool = False, workspace: torch.Tensor = None):
+    """NEXT-2: region labels from a [3, H, W] / [B, 3, H, W] f32
+    normal image.  Returns (labels int32 [.., H, W], n_regions int32 [B],
+    edge mask uint8 [.., H, W] or None)."""
+    if not normals.is_cuda or normals.dtype != torch.float32 or not normals.is_contiguous():
+        raise PMError("pmap: expected a contiguous CUDA float32 normal image")
+    single = normals.dim() == 3
+    n4 = normals.unsqueeze(0) if single else normals
+    B, C, H, W = n4.shape
+    if C != 3:
+        raise PMError("pmap: expected 3 normal channels")
+    dev = normals.device
+    labels = torch.empty(B, H, W, dtype=torch.int32, device=dev)
+    nreg = torch.empty(B, dtype=torch.int32, device=dev)
+    emask = torch.empty(B, H, W, dtype=torch.uint8, device=dev) if edges else None
+    ws = workspace if workspace is not None else _workspace(segment_workspace_bytes(W, H, B, min_area), dev)
+    prm = pm_segment_params(float(canny_low), float(canny_high), int(min_area), int(max_regions))
+    _check(_lib.pm_segment_regions(n4.data_ptr(), W, H, B, ctypes.byref(prm), labels.data_ptr(), nreg.data_ptr(),
+                                   emask.data_ptr() if edges else None, ws.data_ptr(), ws.numel(), _stream(normals)))
+    if single:
+        labels = labels[0]
+        emask = emask[0] if edges else None
+    return labels, nreg, emask

@@ -356,3 +356,36 @@ def test_stream_engine_bitwise_equals_tiled(pm, name, kw):
     d_in = fr["depth"].numpy()
     _check_depth(out.cpu().numpy(), d_in, oracle.adf(d_in, fr["lam"], fr["kappa"], it))
     _check_normals(nrm.cpu().numpy(), oracle.normals(out.cpu().numpy(), fr["K"]))
+
+
+# --------------------------------------------- NEXT-2: labels from normals
+@pytest.mark.parametrize("name,kw", [("C1n", {}), ("C2", {}), ("C2", {"noise": False}), ("C2", {"holes": 0.01}),
+                                     ("C2", {"W": 333, "H": 251}), ("C3", {})])
+def test_segment_regions_bit_exact(pm, name, kw):
+    fr = scenegen.make_config(name, **kw)
+    d_out, nrm = pm.adf_filter(fr["depth"].to(DEV), fr["K"], fr["lam"], fr["kappa"], fr["iters"])
+    min_area = 300 if fr["W"] >= 320 else 20
+    labels, nreg, edges = pm.segment_regions(nrm, 30, 90, min_area, 1024, edges=True)
+    torch.cuda.synchronize()
+    ref_lab, ref_n, ref_e = oracle.segment_regions(nrm.cpu().numpy(), 30, 90, min_area, 1024)
+    assert np.array_equal(edges.cpu().numpy(), ref_e)
+    assert int(nreg[0]) == ref_n
+    assert np.array_equal(labels.cpu().numpy(), ref_lab)
+
+
+def test_segment_then_ransac_pipeline(pm):
+    """depth -> ADF + normals -> segmentation -> RANSAC, all on the device,
+    batched; bit-exact against the oracle chain on the GPU's buffers."""
+    d, _, K = scenegen.stair_stream(40, 3, 320, 240, 8)
+    dev_d = d.to(DEV)
+    d_out, nrm = pm.adf_filter(dev_d, K, 0.15, 0.03, 20)
+    labels, nreg, _ = pm.segment_regions(nrm, 30, 90, 200, 64)
+    planes = pm.ransac_planes(d_out, K, labels, 64, 64, 0.01, 3, first_frame_id=40)
+    torch.cuda.synchronize()
+    for i in range(3):
+        ref_lab, ref_n, _ = oracle.segment_regions(nrm[i].cpu().numpy(), 30, 90, 200, 64)
+        assert np.array_equal(labels[i].cpu().numpy(), ref_lab) and int(nreg[i]) == ref_n
+        ref = oracle.ransac(d_out[i].cpu().numpy(), ref_lab, K, 64, 64, 0.01, 3, frame_id=40 + i)
+        assert np.array_equal(planes.best_hyp[i].cpu().numpy(), ref["best_hyp"])
+        assert np.array_equal(planes.status[i].cpu().numpy(), ref["status"])
+        assert (ref["status"][:ref_n] == 0).mean() > 0.5
