@@ -220,13 +220,87 @@ seg_dilate(const uint8_t* __restrict__ e0, int W, int H, uint8_t* __restrict__ e
     e1[f * HW + i] = any;
 }
 
+// component sizes; neighbouring pixels share roots, so lanes with the same
+// root combine their increments first (one atomic per root per warp)
 __global__ void __launch_bounds__(kT)
 seg_sizes(int HW, const int* __restrict__ parent, int* __restrict__ size) {
     const size_t i = (size_t)blockIdx.x * kT + threadIdx.x;
     const size_t f = blockIdx.y;
-    if (i >= (size_t)HW) return;
-    const int r = parent[f * HW + i];
-    if (r >= 0) atomicAdd(size + f * HW + r, 1);
+    const int r = i < (size_t)HW ? parent[f * HW + i] : -1;
+    const unsigned m = __match_any_sync(0xFFFFFFFFu, r);
+    if (r >= 0 && (int)(threadIdx.x & 31) == __ffs(m) - 1) atomicAdd(size + f * HW + r, __popc(m));
+}
+
+// Block-local labelling of the non-edge pixels (4-connectivity) of a
+// 32 x 32 tile in shared memory, then the global parent of every pixel is the
+// global index of its tile-local root (the tile's smallest raster index of
+// that piece: tile-local order is monotone in global raster order).  Only
+// pixels on the tile's west / north border are merged globally afterwards.
+constexpr int kCT = 32;
+PM_DEVINL int l_find(const int* lp, int p) {
+    int q = lp[p];
+    while (q != p) { p = q; q = lp[p]; }
+    return p;
+}
+PM_DEVINL void l_unite(int* lp, int a, int b) {
+    while (true) {
+        a = l_find(lp, a);
+        b = l_find(lp, b);
+        if (a == b) return;
+        if (a > b) { const int t = a; a = b; b = t; }
+        const int old = atomicMin(lp + b, a);
+        if (old == b) return;
+        b = old;
+    }
+}
+
+__global__ void __launch_bounds__(256)
+seg_local_ccl4(const uint8_t* __restrict__ edge, int W, int H, int* __restrict__ parent) {
+    __shared__ int lp[kCT * kCT];
+    const size_t f = blockIdx.z;
+    const size_t HW = (size_t)W * H;
+    const int x0 = blockIdx.x * kCT, y0 = blockIdx.y * kCT;
+    const uint8_t* e = edge + f * HW;
+    for (int i = threadIdx.x; i < kCT * kCT; i += 256) {
+        const int ly = i / kCT, lx = i % kCT;
+        const int gy = y0 + ly, gx = x0 + lx;
+        lp[i] = (gy < H && gx < W && e[(size_t)gy * W + gx] == 0) ? i : -1;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < kCT * kCT; i += 256) {
+        if (lp[i] < 0) continue;
+        const int ly = i / kCT, lx = i % kCT;
+        if (lx > 0 && lp[i - 1] >= 0) l_unite(lp, i, i - 1);
+        if (ly > 0 && lp[i - kCT] >= 0) l_unite(lp, i, i - kCT);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < kCT * kCT; i += 256) {
+        const int ly = i / kCT, lx = i % kCT;
+        const int gy = y0 + ly, gx = x0 + lx;
+        if (gy >= H || gx >= W) continue;
+        int g = -1;
+        if (lp[i] >= 0) {
+            const int r = l_find(lp, i);
+            g = (y0 + r / kCT) * W + (x0 + r % kCT);
+        }
+        parent[f * HW + (size_t)gy * W + gx] = g;
+    }
+}
+
+// global merge across tile borders (west column and north row of each tile)
+__global__ void __launch_bounds__(kT)
+seg_border_merge4(int W, int H, int* __restrict__ parent) {
+    const size_t i = (size_t)blockIdx.x * kT + threadIdx.x;
+    const size_t f = blockIdx.y;
+    const size_t HW = (size_t)W * H;
+    if (i >= HW) return;
+    const int v = (int)(i / W), u = (int)(i % W);
+    const bool west = u > 0 && (u % kCT) == 0, north = v > 0 && (v % kCT) == 0;
+    if (!west && !north) return;
+    int* par = parent + f * HW;
+    if (__ldcg(par + i) < 0) return;
+    if (west && __ldcg(par + i - 1) >= 0) uf_unite(par, (int)i, (int)i - 1);
+    if (north && __ldcg(par + i - W) >= 0) uf_unite(par, (int)i, (int)(i - W));
 }
 
 // roots of components with >= min_area pixels -> key list; every root's rank = -1
@@ -347,9 +421,9 @@ PM_API pm_status pm_segment_regions(const float* normals, int32_t W, int32_t H, 
     seg_strong<<<gp, kT, 0, s>>>(L.cls, HW, L.parent, L.aux);
     seg_edges<<<gp, kT, 0, s>>>(L.cls, HW, L.parent, L.aux, L.e0);
     seg_dilate<<<gp, kT, 0, s>>>(L.e0, W, H, L.e1);
-    // regions: 4-connected components of non-edge pixels
-    seg_uf_init<1><<<gp, kT, 0, s>>>(L.e1, HW, L.parent);
-    seg_uf_merge<1><<<gp, kT, 0, s>>>(W, H, L.parent);
+    // regions: 4-connected components of non-edge pixels (tile-local first)
+    seg_local_ccl4<<<dim3((W + kCT - 1) / kCT, (H + kCT - 1) / kCT, n_frames), 256, 0, s>>>(L.e1, W, H, L.parent);
+    seg_border_merge4<<<gp, kT, 0, s>>>(W, H, L.parent);
     seg_uf_flatten<<<gp, kT, 0, s>>>(HW, L.parent);
     if (cudaMemsetAsync(L.aux, 0, sizeof(int) * bytes, s) != cudaSuccess) return PM_ERR_CUDA;
     if (cudaMemsetAsync(L.count, 0, sizeof(int) * n_frames, s) != cudaSuccess) return PM_ERR_CUDA;
