@@ -2,25 +2,30 @@
 NVCC     ?= /usr/local/cuda/bin/nvcc
 PKG      := paper_2411_01919_b200
 SRC      := $(wildcard $(PKG)/csrc/*.cu)
+OBJ      := $(patsubst $(PKG)/csrc/%.cu,build/%.o,$(SRC))
 HDR      := $(wildcard $(PKG)/csrc/*.cuh $(PKG)/csrc/*.h) include/pmap.h
 LIB      := $(PKG)/libpmap.so
 # --fmad=false: no implicit FMA contraction; every fused multiply-add the
 # method prescribes is written as __fmaf_rn.
 NVFLAGS  := -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -lineinfo --fmad=false \
-            -Xcompiler -fPIC,-fvisibility=hidden -shared -Iinclude
+            -Xcompiler -fPIC,-fvisibility=hidden -Iinclude
 
 all: $(LIB) oracle/liboracle.so
 
-$(LIB): $(SRC) $(HDR)
-	$(NVCC) $(NVFLAGS) -o $@.tmp $(SRC) && mv $@.tmp $@
+build/%.o: $(PKG)/csrc/%.cu $(HDR)
+	@mkdir -p build
+	$(NVCC) $(NVFLAGS) -c -o $@ $<
+
+$(LIB): $(OBJ)
+	$(NVCC) -shared -gencode arch=compute_100a,code=sm_100a -o $@.tmp $(OBJ) && mv $@.tmp $@
 
 oracle/liboracle.so: oracle/oracle.c
 	gcc -O2 -std=c11 -fPIC -shared -ffp-contract=off -fno-fast-math -fvisibility=hidden -o $@ $< -lm
 
 ptxas:
-	$(NVCC) $(NVFLAGS) -Xptxas -v -o /tmp/pmap_ptxas.so $(SRC) 2>&1 | grep -E "Function properties|registers|spill|smem|Compiling entry" | sed 's/ptxas info    ://'
+	$(NVCC) $(NVFLAGS) -Xptxas -v -c -o /tmp/pmap_ptxas.o $(F) 2>&1 | grep -E "Function properties|registers|spill|smem|Compiling entry" | sed 's/ptxas info    ://'
 
 clean:
-	rm -f $(LIB) oracle/liboracle.so
+	rm -rf $(LIB) oracle/liboracle.so build
 
 .PHONY: all clean ptxas

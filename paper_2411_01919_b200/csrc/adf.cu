@@ -34,7 +34,7 @@ namespace pm {
 
 namespace {
 
-constexpr int kThreads = 256;      // 8 warps (3 CTAs / SM: shared memory bound)
+constexpr int kThreads = 256;      // 8 warps (4 CTAs / SM for halo R <= 5)
 constexpr int kWarps = kThreads / 32;
 constexpr int kMaxItersPerPass = 16;
 
@@ -43,6 +43,7 @@ struct AdfParams {
     float l2lam;      // log2(lambda): lambda * c = 2^(kc * g2 + log2(lambda))
     float kd;         // -log2(e) / kappa^2 (divergence scheme: c(d) = 2^(kd d^2))
     float lam;
+    float negz;       // -0.0f (run-time operand, see f2mul_nf)
     float fx, fy, cx, cy;
     float ifx, ify;   // 1/fx, 1/fy (Eq. 2 as printed)
     int scheme;       // PM_ADF_ALG1 | PM_ADF_DIVERGENCE
@@ -94,7 +95,10 @@ PM_DEVINL float cell(float C, float N, float S, float W, float E, const AdfParam
 // output tile is (kSW - 2R) x TH; smem cell (sx, sy) is image pixel
 // (x0 + sx, y0 + sy); the image covers smem columns [ix0, ix1), rows [iy0, iy1).
 constexpr int kSW = 128;
-constexpr int kTH = 64;               // output rows per CTA
+// Output rows per CTA.  44: a (44 + 2R)-row tile pair fits 4 CTAs per SM in
+// shared memory for R <= 5 (the default passes), and 480-row frames split
+// into 11 tiles wasting 4 rows (64-row tiles: 8 tiles, 32 wasted rows).
+constexpr int kTH = 44;
 
 struct Box { int ix0, ix1, iy0, iy1; };
 
@@ -136,6 +140,85 @@ PM_DEVINL void sweep(const float* __restrict__ cur, float* __restrict__ nxt, int
         ocol[y * kSW] = cell<CHECK, DIV>(C, N, C, colW[y * kSW], colE[y * kSW], p);
 }
 
+// ---------------------------------------------------------------------------
+// Packed fp32 (sm_100a FADD2 / FMUL2 / FFMA2): one instruction updates both
+// cells of a thread's pair (x, x+1) -- the same FP32-pipe work as two scalar
+// ops in half the issue slots.  With P = (W, E) (the pair's outer neighbours,
+// two scalar loads into one register pair) and Cs = (C.y, C.x) (the pair
+// swapped: a free operand swizzle, .F32x2.LO_HI), the low cell's west / east
+// neighbours are (W, C.y) and the high cell's are (C.x, E), so
+//   Cs - P = (E - W | lo, -(E - W) | hi)   and   P + Cs = (W + E | lo, E + W | hi).
+// The cell formula uses W and E only through (E - W)^2 and W + E, so both
+// cells get exactly the rounding sequence of adf_cell() / adf_cell_div()
+// (bitwise invariance).
+// Packed fp32 ops as inline PTX (the __fmul2_rn/__fadd2_rn intrinsics get
+// contracted into FFMA2 even under --fmad=false: measured, the divergence
+// scheme lost bitwise equality with the scalar path).
+PM_DEVINL uint64_t f2pk(float2 a) {
+    uint64_t r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a.x), "f"(a.y));
+    return r;
+}
+PM_DEVINL float2 f2up(uint64_t r) {
+    float2 a;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a.x), "=f"(a.y) : "l"(r));
+    return a;
+}
+PM_DEVINL float2 f2add(float2 a, float2 b) {
+    uint64_t r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2pk(a)), "l"(f2pk(b)));
+    return f2up(r);
+}
+PM_DEVINL float2 f2sub(float2 a, float2 b) {
+    uint64_t r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2pk(a)), "l"(f2pk(b)));
+    return f2up(r);
+}
+PM_DEVINL float2 f2mul(float2 a, float2 b) {
+    uint64_t r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2pk(a)), "l"(f2pk(b)));
+    return f2up(r);
+}
+PM_DEVINL float2 f2fma(float2 a, float2 b, float2 c) {
+    uint64_t r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(f2pk(a)), "l"(f2pk(b)), "l"(f2pk(c)));
+    return f2up(r);
+}
+PM_DEVINL float2 f2s(float a) { return make_float2(a, a); }
+// A product that feeds an add: ptxas fuses mul.rn.f32x2 + add.rn.f32x2 into
+// FFMA2 even under --fmad=false (measured), and folds fma(a, b, -0) back into
+// a mul.  fma(a, b, z) with z = -0 passed in at run time is the same rounded
+// product for every input (a -0 addend keeps the sign of a zero product) and
+// cannot be fused with the add.
+PM_DEVINL float2 f2mul_nf(float2 a, float2 b, float z) { return f2fma(a, b, f2s(z)); }
+
+PM_DEVINL float2 adf_cell2(float2 C, float2 N, float2 S, float2 Wv, float2 Ev, float kc, float l2lam) {
+    const float2 gx2 = f2sub(Ev, Wv);
+    const float2 gy2 = f2sub(S, N);
+    const float2 g2 = f2fma(gx2, gx2, f2mul(gy2, gy2));
+    const float2 e = f2fma(g2, f2s(kc), f2s(l2lam));
+    const float2 lc = make_float2(ex2_approx(e.x), ex2_approx(e.y));
+    const float2 lap = f2fma(f2s(-4.0f), C, f2add(f2add(N, S), f2add(Wv, Ev)));
+    return f2fma(lc, lap, C);
+}
+
+PM_DEVINL float2 flux2(float2 d, float kd, float z) {
+    const float2 a = f2mul(f2mul(d, d), f2s(kd));
+    return f2mul_nf(make_float2(ex2_approx(a.x), ex2_approx(a.y)), d, z);
+}
+
+PM_DEVINL float2 adf_cell2_div(float2 C, float2 N, float2 S, float2 Wv, float2 Ev, float kd, float lam, float z) {
+    const float2 fn = flux2(f2sub(N, C), kd, z), fs = flux2(f2sub(S, C), kd, z);
+    const float2 fw = flux2(f2sub(Wv, C), kd, z), fe = flux2(f2sub(Ev, C), kd, z);
+    return f2fma(f2s(lam), f2add(f2add(fn, fs), f2add(fw, fe)), C);
+}
+
+template <bool DIV>
+PM_DEVINL float2 cell2(float2 C, float2 N, float2 S, float2 Wv, float2 Ev, const AdfParams& p) {
+    return DIV ? adf_cell2_div(C, N, S, Wv, Ev, p.kd, p.lam, p.negz) : adf_cell2(C, N, S, Wv, Ev, p.kc, p.l2lam);
+}
+
+
 // Same sweep with two horizontally adjacent cells per thread (columns x, x+1,
 // x even): per row one 8-byte load of the south pair, one load each for the
 // outer west / east neighbours (the inner ones are the pair itself), one
@@ -160,32 +243,71 @@ PM_DEVINL void sweep_pairs(const float* __restrict__ cur, float* __restrict__ nx
     const int ymid = min(ye, ylast);
     const int offW = x == b.ix0 ? 0 : -1;           // zero flux at the image border (Q4)
     const int offE = x + 2 == b.ix1 ? 1 : 2;
-    const float* col = cur + x;
-    const float* colW = col + offW;
-    const float* colE = col + offE;
-    float* ocol = nxt + x;
-    float2 C = *reinterpret_cast<const float2*>(col + ys * kSW);
-    float2 N = ys == b.iy0 ? C : *reinterpret_cast<const float2*>(col + (ys - 1) * kSW);
+    const float* __restrict__ col = cur + x + ys * kSW;
+    const float* __restrict__ colW = col + offW;
+    const float* __restrict__ colE = col + offE;
+    float* __restrict__ ocol = nxt + x + ys * kSW;
+    auto ld2 = [](const float* a) { return *reinterpret_cast<const float2*>(a); };
+    float2 C = ld2(col);
+    float2 N = ys == b.iy0 ? C : ld2(col - kSW);
+    if (!CHECK) {
+        // packed path, software-pipelined: the next row's S, W, E are loaded
+        // before this row's store (loads are not hoisted above a possibly
+        // aliasing store).  The last step prefetches one row past the region
+        // (at most row SH: the buffers carry one spare row), never used.
+        const int n = ymid - ys;
+        float2 S = ld2(col + kSW);
+        float2 P = make_float2(colW[0], colE[0]);
+        auto step = [&]() {
+            const float2 S1 = ld2(col + 2 * kSW);
+            const float2 P1 = make_float2(colW[kSW], colE[kSW]);
+            *reinterpret_cast<float2*>(ocol) = cell2<DIV>(C, N, S, P, make_float2(C.y, C.x), p);
+            N = C;
+            C = S;
+            S = S1;
+            P = P1;
+            col += kSW;
+            colW += kSW;
+            colE += kSW;
+            ocol += kSW;
+        };
+        int i = 0;
+        for (; i + 4 <= n; i += 4) {
+            step(); step(); step(); step();
+        }
+        if (i < n) {                                // 0-3 last rows, straight-line
+            step();
+            if (i + 1 < n) {
+                step();
+                if (i + 2 < n) step();
+            }
+        }
+        if (ye > ylast)                           // last image row: S = C
+            *reinterpret_cast<float2*>(ocol) = cell2<DIV>(C, N, C, P, make_float2(C.y, C.x), p);
+        return;
+    }
     int y = ys;
 #pragma unroll 4
     for (; y < ymid; ++y) {
-        const float2 S = *reinterpret_cast<const float2*>(col + (y + 1) * kSW);
-        const float W = colW[y * kSW];
-        const float E = colE[y * kSW];
+        const float2 S = ld2(col + kSW);
+        const float W = colW[0];
+        const float E = colE[0];
         float2 o;
         o.x = cell<CHECK, DIV>(C.x, N.x, S.x, W, C.y, p);
         o.y = cell<CHECK, DIV>(C.y, N.y, S.y, C.x, E, p);
-        *reinterpret_cast<float2*>(ocol + y * kSW) = o;
+        *reinterpret_cast<float2*>(ocol) = o;
         N = C;
         C = S;
+        col += kSW;
+        colW += kSW;
+        colE += kSW;
+        ocol += kSW;
     }
     if (ye > ylast) {                               // last image row: S = C
-        const float W = colW[y * kSW];
-        const float E = colE[y * kSW];
         float2 o;
-        o.x = cell<CHECK, DIV>(C.x, N.x, C.x, W, C.y, p);
-        o.y = cell<CHECK, DIV>(C.y, N.y, C.y, C.x, E, p);
-        *reinterpret_cast<float2*>(ocol + y * kSW) = o;
+        o.x = cell<CHECK, DIV>(C.x, N.x, C.x, colW[0], C.y, p);
+        o.y = cell<CHECK, DIV>(C.y, N.y, C.y, C.x, colE[0], p);
+        *reinterpret_cast<float2*>(ocol) = o;
     }
 }
 
@@ -222,7 +344,7 @@ PM_DEVINL float3 sobel_normal(const float z[3][3], float u, float v, const AdfPa
 }
 
 template <int R>
-constexpr size_t pass_smem_bytes() { return sizeof(float) * 2 * (size_t)kSW * (kTH + 2 * R); }
+constexpr size_t pass_smem_bytes() { return sizeof(float) * ((size_t)2 * kSW * (kTH + 2 * R) + kSW); }
 
 // Left halo rounded up to 4 columns: the TMA box must start on a 16-byte
 // column boundary (measured on B200: other starts raise an illegal-instruction
@@ -235,7 +357,7 @@ __host__ __device__ constexpr int tile_w() { return kSW - 2 * halo_x<R>(); }
 // One pass of `iters` sweeps; halo R = iters (+1 when the normals are fused).
 //   src [B][H][W] -> dst [B][H][W] (if dst) and normals [B][3][H][W] (if normals).
 template <int R, bool DIV>
-__global__ void __launch_bounds__(kThreads, 2)
+__global__ void __launch_bounds__(kThreads, 4)   // <= 64 registers: 4 CTAs / SM
 adf_pass_kernel(const float* __restrict__ src, float* __restrict__ dst, float* __restrict__ normals,
                 int W, int H, int iters, AdfParams p, const __grid_constant__ CUtensorMap tmap, int use_tma,
                 int* __restrict__ frame_flags, int flag_mode) {
@@ -453,6 +575,7 @@ static AdfParams make_params(const pm_intrinsics* K, float lam, float kappa, int
     p.l2lam = (float)log2((double)lam);
     p.kd = (float)(-1.4426950408889634 / ((double)kappa * (double)kappa));
     p.lam = lam;
+    p.negz = -0.0f;
     p.fx = K ? K->fx : 1.f;
     p.fy = K ? K->fy : 1.f;
     p.cx = K ? K->cx : 0.f;
