@@ -151,40 +151,6 @@ PM_DEVINL void sweep(const float* __restrict__ cur, float* __restrict__ nxt, int
 // The cell formula uses W and E only through (E - W)^2 and W + E, so both
 // cells get exactly the rounding sequence of adf_cell() / adf_cell_div()
 // (bitwise invariance).
-// Packed fp32 ops as inline PTX (the __fmul2_rn/__fadd2_rn intrinsics get
-// contracted into FFMA2 even under --fmad=false: measured, the divergence
-// scheme lost bitwise equality with the scalar path).
-PM_DEVINL uint64_t f2pk(float2 a) {
-    uint64_t r;
-    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a.x), "f"(a.y));
-    return r;
-}
-PM_DEVINL float2 f2up(uint64_t r) {
-    float2 a;
-    asm("mov.b64 {%0, %1}, %2;" : "=f"(a.x), "=f"(a.y) : "l"(r));
-    return a;
-}
-PM_DEVINL float2 f2add(float2 a, float2 b) {
-    uint64_t r;
-    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2pk(a)), "l"(f2pk(b)));
-    return f2up(r);
-}
-PM_DEVINL float2 f2sub(float2 a, float2 b) {
-    uint64_t r;
-    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2pk(a)), "l"(f2pk(b)));
-    return f2up(r);
-}
-PM_DEVINL float2 f2mul(float2 a, float2 b) {
-    uint64_t r;
-    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2pk(a)), "l"(f2pk(b)));
-    return f2up(r);
-}
-PM_DEVINL float2 f2fma(float2 a, float2 b, float2 c) {
-    uint64_t r;
-    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(f2pk(a)), "l"(f2pk(b)), "l"(f2pk(c)));
-    return f2up(r);
-}
-PM_DEVINL float2 f2s(float a) { return make_float2(a, a); }
 // A product that feeds an add: ptxas fuses mul.rn.f32x2 + add.rn.f32x2 into
 // FFMA2 even under --fmad=false (measured), and folds fma(a, b, -0) back into
 // a mul.  fma(a, b, z) with z = -0 passed in at run time is the same rounded

@@ -16,6 +16,43 @@ constexpr int kWarp = 32;
 // Depth validity (Q4 / S:69): > 0 and finite.  Positive finite floats are the
 // bit patterns [0x00000001, 0x7F7FFFFF]; one unsigned compare covers 0, -0,
 // negatives, inf and NaN.
+// ---- packed fp32 pairs (sm_100a FADD2 / FMUL2 / FFMA2: two fp32 lanes per
+// instruction, the FP32-pipe work of two scalar ops in one issue slot).
+// Packed fp32 ops as inline PTX (the __fmul2_rn/__fadd2_rn intrinsics get
+// contracted into FFMA2 even under --fmad=false: measured, the divergence
+// scheme lost bitwise equality with the scalar path).
+PM_DEVINL uint64_t f2pk(float2 a) {
+    uint64_t r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a.x), "f"(a.y));
+    return r;
+}
+PM_DEVINL float2 f2up(uint64_t r) {
+    float2 a;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a.x), "=f"(a.y) : "l"(r));
+    return a;
+}
+PM_DEVINL float2 f2add(float2 a, float2 b) {
+    uint64_t r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2pk(a)), "l"(f2pk(b)));
+    return f2up(r);
+}
+PM_DEVINL float2 f2sub(float2 a, float2 b) {
+    uint64_t r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2pk(a)), "l"(f2pk(b)));
+    return f2up(r);
+}
+PM_DEVINL float2 f2mul(float2 a, float2 b) {
+    uint64_t r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2pk(a)), "l"(f2pk(b)));
+    return f2up(r);
+}
+PM_DEVINL float2 f2fma(float2 a, float2 b, float2 c) {
+    uint64_t r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(f2pk(a)), "l"(f2pk(b)), "l"(f2pk(c)));
+    return f2up(r);
+}
+PM_DEVINL float2 f2s(float a) { return make_float2(a, a); }
+
 PM_DEVINL bool valid_depth(float z) { return (__float_as_uint(z) - 1u) < 0x7F7FFFFFu; }
 
 // exp2 on the MUFU unit (flush-to-zero; c_p underflows harmlessly to 0).

@@ -37,12 +37,14 @@ struct Sums;
 struct RansacWorkspace {
     // sizes
     int W, H, B, R, n_hyp, n_hyp_pad, sub_tile, n_sub, n_slots;
+    int score_K, score_L;  // scoring layout: K hypotheses per lane, L lanes per group (K * L >= n_hyp)
     // buffers (device)
     uint2* points;        // [B][W*H] packed (u | v<<16, z bits), region-major, raster order
     int32_t* hist;        // [B][R][n_sub] count -> exclusive prefix per region
     int32_t* region_cnt;  // [B][R]
     int32_t* region_off;  // [B][R+1]
     float4* planes;       // [B][R][n_hyp_pad] hypothesis planes (NaN = invalid)
+    float2* pairs;        // [B][R][K/2][L][4] plane pairs (h, h + L) per component, for packed scoring
     int32_t* counts;      // [B][R][n_hyp_pad] inlier counts (-1 = invalid)
     uint64_t* errq;       // [B][R][n_hyp_pad] fixed-point error sums (select=ERROR / debug)
     Sums* slots;          // [B][n_slots] refit moments per (region, chunk): slot chunk + region

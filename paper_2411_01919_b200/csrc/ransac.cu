@@ -96,9 +96,10 @@ PM_DEVINL bool plane_from_3pts(float3 p0, float3 p1, float3 p2, float4& pl) {
 __global__ void __launch_bounds__(256)
 ransac_hyp_kernel(RansacWorkspace ws, RansacArgs a, int need_err) {
     const int idx = blockIdx.x * 256 + threadIdx.x;
-    const int R = ws.R, HP = ws.n_hyp_pad;
-    if (idx >= R * HP) return;
-    const int r = idx / HP, h = idx % HP;
+    const int R = ws.R, HP = ws.n_hyp_pad, KL = ws.score_K * ws.score_L;
+    const int HS = max(HP, KL);
+    if (idx >= R * HS) return;
+    const int r = idx / HS, h = idx % HS;
     const size_t f = blockIdx.y;
     const size_t slot = (f * R + r) * HP + h;
     const int32_t* off = ws.region_off + f * (size_t)(R + 1);
@@ -118,9 +119,19 @@ ransac_hyp_kernel(RansacWorkspace ws, RansacArgs a, int need_err) {
             if (plane_from_3pts(p0, p1, p2, t)) { pl = t; c0 = 0; }
         }
     }
-    ws.planes[slot] = pl;
-    ws.counts[slot] = c0;
-    if (need_err) ws.errq[slot] = 0ull;
+    if (h < HP) {
+        ws.planes[slot] = pl;
+        ws.counts[slot] = c0;
+        if (need_err) ws.errq[slot] = 0ull;
+    }
+    if ((ws.score_K & 1) == 0 && h < KL) {      // packed-scoring copy: pair (h, h + L) per component
+        const int L = ws.score_L, k = h / L, l = h % L, j = k >> 1, half = k & 1;
+        float* q = reinterpret_cast<float*>(ws.pairs) + ((f * R + r) * (size_t)(2 * KL) + (j * L + l) * 4) * 2 + half;
+        q[0] = pl.x;
+        q[2] = pl.y;
+        q[4] = pl.z;
+        q[6] = pl.w;
+    }
 }
 
 // ---- chunk staging shared by the score and refit kernels: the compacted
@@ -164,6 +175,15 @@ PM_DEVINL void count_lt(int& c, float a, float b) {
     asm("{\n.reg .pred p;\nsetp.lt.f32 p, %1, %2;\n@p add.s32 %0, %0, 1;\n}" : "+r"(c) : "f"(a), "f"(b));
 }
 
+// Packed-pair scoring (two hypotheses per FFMA2 chain) for even K without the
+// error sum, reading the plane pairs the hyp kernel lays out (ws.pairs).
+template <int K, int L, bool WITH_ERR>
+__host__ __device__ constexpr bool score_packed() { return !WITH_ERR && (K % 2) == 0; }
+template <int K, int L, bool WITH_ERR>
+constexpr size_t score_smem_bytes() {
+    return sizeof(float4) * kScoreChunk + sizeof(int) * kScoreThreads * K;
+}
+
 // The hot loop (Alg. 2 ℓ9-13).  grid = (ceil(W*H / kScoreChunk), B).  The CTA's
 // threads form G = 256 / L groups of L lanes; lane l of every group holds
 // hypotheses l, l + L, ..., l + (K-1) L of the current region in registers;
@@ -199,19 +219,71 @@ ransac_score_kernel(RansacWorkspace ws, RansacArgs a) {
 #pragma unroll
         for (int k = 0; k < K; ++k) {
             const int h = l + k * L;
-            pl[k] = h < NH ? __ldg(planes + h) : nan4;
+            pl[k] = (!score_packed<K, L, WITH_ERR>() && h < NH) ? __ldg(planes + h) : nan4;
             c[k] = 0;
             eq[k] = 0;
         }
+        if (!score_packed<K, L, WITH_ERR>()) {
 #pragma unroll 4
-        for (int i = lo + g; i < hi; i += G) {
-            const float4 p4 = sp[i];
-            const float3 P = make_float3(p4.x, p4.y, p4.z);
+            for (int i = lo + g; i < hi; i += G) {
+                const float4 p4 = sp[i];
+                const float3 P = make_float3(p4.x, p4.y, p4.z);
 #pragma unroll
-            for (int k = 0; k < K; ++k) {
-                const float dist = plane_dist(pl[k], P);
-                count_lt(c[k], dist, tau);
-                if (WITH_ERR) eq[k] += __float2ull_rn(__fmul_rn(fminf(dist, 64.0f), 16777216.0f));
+                for (int k = 0; k < K; ++k) {
+                    const float dist = plane_dist(pl[k], P);
+                    count_lt(c[k], dist, tau);
+                    if (WITH_ERR) eq[k] += __float2ull_rn(__fmul_rn(fminf(dist, 64.0f), 16777216.0f));
+                }
+            }
+        } else {
+            // two hypotheses per packed FFMA2 chain: the same per-lane fma
+            // sequence as plane_dist(), so the counts stay bit-exact
+            // plane pairs as written by the hyp kernel ([K/2][L] x (x, y, z, w)
+            // pairs): they reach the registers as 64-bit pairs (pairs built from
+            // scalars get re-paired with moves on every use)
+            constexpr int K2 = K / 2 > 0 ? K / 2 : 1;
+            const ulonglong2* pp = reinterpret_cast<const ulonglong2*>(ws.pairs) + (f * R + r) * (size_t)(K * L);
+            uint64_t X[K2], Y[K2], Z[K2], D[K2];
+#pragma unroll
+            for (int j = 0; j < K2; ++j) {
+                const ulonglong2 u = __ldg(pp + (j * L + l) * 2);
+                const ulonglong2 v = __ldg(pp + (j * L + l) * 2 + 1);
+                X[j] = u.x; Y[j] = u.y; Z[j] = v.x; D[j] = v.y;
+            }
+            // inlier indicators as 1.0f / 0.0f (FSET, NaN -> 0) summed two at a
+            // time (FADD2); exact: a thread adds at most kScoreChunk ones
+            uint64_t acc[K2];
+#pragma unroll
+            for (int j = 0; j < K2; ++j) acc[j] = 0ull;
+#pragma unroll 4
+            for (int i = lo + g; i < hi; i += G) {
+                const float4 p4 = sp[i];
+                const uint64_t px = f2pk(f2s(p4.x)), py = f2pk(f2s(p4.y)), pz = f2pk(f2s(p4.z));
+#pragma unroll
+                for (int j = 0; j < K2; ++j) {
+                    uint64_t d;
+                    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(X[j]), "l"(px), "l"(D[j]));
+                    asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(d) : "l"(Y[j]), "l"(py));
+                    asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(d) : "l"(Z[j]), "l"(pz));
+                    const float2 df = f2up(d);
+                    if (j & 1) {
+                        // odd pairs count on the ALU pipe (FSETP + predicated IADD),
+                        // even pairs on the FMA pipe (FADD2): both pipes stay busy
+                        count_lt(c[2 * j], fabsf(df.x), tau);
+                        count_lt(c[2 * j + 1], fabsf(df.y), tau);
+                    } else {
+                        float i0, i1;
+                        asm("set.lt.f32.f32 %0, %1, %2;" : "=f"(i0) : "f"(fabsf(df.x)), "f"(tau));
+                        asm("set.lt.f32.f32 %0, %1, %2;" : "=f"(i1) : "f"(fabsf(df.y)), "f"(tau));
+                        asm("add.rn.f32x2 %0, %0, %1;" : "+l"(acc[j]) : "l"(f2pk(make_float2(i0, i1))));
+                    }
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < K2; j += 2) {
+                const float2 a2 = f2up(acc[j]);
+                c[2 * j] = (int)a2.x;
+                c[2 * j + 1] = (int)a2.y;
             }
         }
         if (WITH_ERR) {
@@ -229,12 +301,26 @@ ransac_score_kernel(RansacWorkspace ws, RansacArgs a) {
                 if (h < NH && c[k] > 0) atomicAdd(counts + h, c[k]);
             }
         } else {
+            // groups of one warp first meet by shuffles (L < 32), then one
+            // partial per warp (or per group) in shared memory
+            constexpr int NP = L < 32 ? kScoreThreads / 32 : G;   // partials per hypothesis
+            const int lane = threadIdx.x & 31;
+            if (L < 32) {
 #pragma unroll
-            for (int k = 0; k < K; ++k) s_cnt[g * (L * K) + k * L + l] = c[k];
+                for (int k = 0; k < K; ++k)
+#pragma unroll
+                    for (int o = L; o < 32; o <<= 1) c[k] += __shfl_xor_sync(kFull, c[k], o);
+            }
+            if (L >= 32 || lane < L) {
+                const int q = L < 32 ? (int)(threadIdx.x >> 5) : g;
+#pragma unroll
+                for (int k = 0; k < K; ++k) s_cnt[q * (L * K) + k * L + l] = c[k];
+            }
             __syncthreads();
             for (int h = threadIdx.x; h < L * K; h += kScoreThreads) {
                 int sum = 0;
-                for (int q = 0; q < G; ++q) sum += s_cnt[q * (L * K) + h];
+#pragma unroll 8
+                for (int q = 0; q < NP; ++q) sum += s_cnt[q * (L * K) + h];
                 if (h < NH && sum > 0) atomicAdd(counts + h, sum);
             }
             __syncthreads();
@@ -504,7 +590,7 @@ cudaError_t ransac_setup_attributes() {
         e = cudaFuncSetAttribute(wr ? (const void*)ransac_score_kernel<KK, LL, true>                        \
                                     : (const void*)ransac_score_kernel<KK, LL, false>,                      \
                                  cudaFuncAttributeMaxDynamicSharedMemorySize,                              \
-                                 (int)(sizeof(float4) * kScoreChunk + sizeof(int) * kScoreThreads * KK));
+                                 (int)(wr ? score_smem_bytes<KK, LL, true>() : score_smem_bytes<KK, LL, false>()));
     PM_ATTR(1, 8) PM_ATTR(2, 8) PM_ATTR(4, 8) PM_ATTR(8, 8) PM_ATTR(8, 16) PM_ATTR(8, 32)
     PM_ATTR(8, 64) PM_ATTR(8, 128) PM_ATTR(8, 256) PM_ATTR(16, 256)
 #undef PM_ATTR
@@ -515,6 +601,13 @@ RansacWorkspace ransac_workspace_layout(void* base, int W, int H, int R, int n_h
     RansacWorkspace ws{};
     ws.W = W; ws.H = H; ws.B = B; ws.R = R; ws.n_hyp = n_hyp;
     ws.n_hyp_pad = ((n_hyp + kHB - 1) / kHB) * kHB;
+    // scoring layout: K hypotheses per lane, L lanes per group (L * K >= n_hyp);
+    // small L means more points in flight per warp, cheaper per-point overhead
+    auto pow2ceil = [](int x) { int p = 1; while (p < x) p <<= 1; return p; };
+    int L = pow2ceil((n_hyp + 7) / 8);
+    L = L < 8 ? 8 : (L > 256 ? 256 : L);
+    ws.score_L = L;
+    ws.score_K = pow2ceil((n_hyp + L - 1) / L);     // <= 8 except n_hyp > 2048 -> 16
     const size_t WH = (size_t)W * H;
     int st = 1024;
     while (st < 4 * R && st < (1 << 24)) st <<= 1;      // hist entries <= ~W*H/4 per frame
@@ -530,6 +623,7 @@ RansacWorkspace ransac_workspace_layout(void* base, int W, int H, int R, int n_h
     ws.region_cnt = (int32_t*)take(sizeof(int32_t) * B * Rm);
     ws.region_off = (int32_t*)take(sizeof(int32_t) * B * (Rm + 1));
     ws.planes = (float4*)take(sizeof(float4) * B * Rm * ws.n_hyp_pad);
+    ws.pairs = (float2*)take(sizeof(float4) * B * Rm * (size_t)ws.score_K * ws.score_L);
     ws.counts = (int32_t*)take(sizeof(int32_t) * B * Rm * ws.n_hyp_pad);
     ws.errq = (uint64_t*)take(sizeof(uint64_t) * B * Rm * ws.n_hyp_pad);
     ws.slots = (Sums*)take(sizeof(Sums) * B * (size_t)ws.n_slots);
@@ -541,21 +635,19 @@ RansacWorkspace ransac_workspace_layout(void* base, int W, int H, int R, int n_h
 cudaError_t ransac_run(const RansacWorkspace& ws, const RansacArgs& a, pm_plane* planes,
                        cudaStream_t stream) {
     const bool need_err = a.select == PM_SELECT_ERROR || a.errq_out != nullptr;
-    const int n_hyp_slots = ws.R * ws.n_hyp_pad;
+    const int K = ws.score_K, L = ws.score_L;
+    const int n_hyp_slots = ws.R * (ws.n_hyp_pad > K * L ? ws.n_hyp_pad : K * L);
     ransac_hyp_kernel<<<dim3((n_hyp_slots + 255) / 256, ws.B), 256, 0, stream>>>(ws, a, need_err ? 1 : 0);
-    // K hypotheses per lane, L lanes per group (L * K >= n_hyp): small L
-    // means more points in flight per warp and a cheaper per-point overhead
-    auto pow2ceil = [](int x) { int p = 1; while (p < x) p <<= 1; return p; };
-    int L = pow2ceil((ws.n_hyp + 7) / 8);
-    L = L < 8 ? 8 : (L > 256 ? 256 : L);
-    const int K = pow2ceil((ws.n_hyp + L - 1) / L);     // <= 8 except n_hyp > 2048 -> 16
     const dim3 g_score((unsigned)(((size_t)ws.W * ws.H + kScoreChunk - 1) / kScoreChunk), ws.B);
-    const size_t smem = sizeof(float4) * kScoreChunk + sizeof(int) * kScoreThreads * K;
     bool launched = false;
 #define PM_SCORE(KK, LL)                                                                                   \
     if (K == KK && L == LL) {                                                                              \
-        if (need_err) ransac_score_kernel<KK, LL, true><<<g_score, kScoreThreads, smem, stream>>>(ws, a);  \
-        else ransac_score_kernel<KK, LL, false><<<g_score, kScoreThreads, smem, stream>>>(ws, a);          \
+        if (need_err)                                                                                      \
+            ransac_score_kernel<KK, LL, true>                                                              \
+                <<<g_score, kScoreThreads, score_smem_bytes<KK, LL, true>(), stream>>>(ws, a);             \
+        else                                                                                               \
+            ransac_score_kernel<KK, LL, false>                                                             \
+                <<<g_score, kScoreThreads, score_smem_bytes<KK, LL, false>(), stream>>>(ws, a);            \
         launched = true;                                                                                   \
     }
     PM_SCORE(1, 8) PM_SCORE(2, 8) PM_SCORE(4, 8) PM_SCORE(8, 8) PM_SCORE(8, 16) PM_SCORE(8, 32)
