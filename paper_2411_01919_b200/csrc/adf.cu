@@ -2,17 +2,18 @@
 // temporally blocked Perona–Malik diffusion (ℓ1-8) with the Sobel/normal
 // stage (ℓ9-13) fused into the last pass.
 //
-// One CTA owns an output tile of (128 - 2R) x 64 pixels of one frame.  It
+// One CTA owns an output tile of (128 - 2RA) x 44 pixels of one frame.  It
 // loads the tile plus an R-pixel halo (R = sweeps of this pass, +1 when the
-// normal stage is fused) into shared memory once, runs the pass's T Jacobi
-// sweeps in shared memory on a region that shrinks by one pixel per sweep
-// (ping-pong buffers), and writes the tile back: one HBM read and one write
-// per T sweeps.
+// normal stage is fused; RA = R rounded up to 4 columns) into shared memory
+// once with one TMA box, runs the pass's T Jacobi sweeps in shared memory on
+// a region that shrinks by one pixel per sweep (ping-pong buffers), and
+// writes the tile back: one HBM read and one write per T sweeps.
 //
-// Sweep inner loop ("column walk"): each thread owns one column of a row
-// strip and walks down it keeping the north and centre values in registers,
-// so a cell update costs 3 shared loads (S, W, E), 1 store, 12 FP32 ops and
-// one MUFU.EX2.  The zero-flux image border (Q4) costs nothing per cell: a
+// Sweep inner loop ("column walk"): each thread owns a pair of adjacent
+// columns of a row strip and walks down it keeping the north and centre pairs
+// in registers; per row and pair: 3 shared loads (S pair, W, E), 1 store, 10
+// packed FP32 instructions (FADD2/FMUL2/FFMA2, see below) and two MUFU.EX2,
+// the next row's loads issued before this row's store.  The zero-flux image border (Q4) costs nothing per cell: a
 // thread whose column is the first / last image column points its W / E
 // address at the centre cell, the strip that starts on the first image row
 // seeds N with the centre, and the last image row is peeled with S = centre.
@@ -26,6 +27,8 @@
 #include <math.h>
 #include <stdint.h>
 #include <string.h>
+
+#include <type_traits>
 
 #include "common.cuh"
 #include "internal.h"
@@ -280,13 +283,19 @@ PM_DEVINL void sweep_pairs(const float* __restrict__ cur, float* __restrict__ nx
 // Sobel (1/8-normalised, clamp-to-edge) + geometric normal (Eq. 2 read as
 // Q7): m = (fx Gx, fy Gy, -(Z + (u-cx) Gx + (v-cy) Gy)), n = m/|m|; (0,0,0)
 // if any window pixel is invalid (Q9).  z[a][b] = window row a, column b.
+// CHECK = false: the caller knows every window pixel is valid (hole-free tile).
+// NM: the normals mode (PM_NORMALS_*), -1 = read p.nmode.
+template <bool CHECK = true, int NM = -1>
 PM_DEVINL float3 sobel_normal(const float z[3][3], float u, float v, const AdfParams& p) {
-    bool ok = true;
+    if (CHECK) {
+        bool ok = true;
 #pragma unroll
-    for (int a = 0; a < 3; ++a)
+        for (int a = 0; a < 3; ++a)
 #pragma unroll
-        for (int b = 0; b < 3; ++b) ok = ok && valid_depth(z[a][b]);
-    if (!ok) return make_float3(0.f, 0.f, 0.f);
+            for (int b = 0; b < 3; ++b) ok = ok && valid_depth(z[a][b]);
+        if (!ok) return make_float3(0.f, 0.f, 0.f);
+    }
+    const int nmode = NM >= 0 ? NM : p.nmode;
     const float gx = __fmul_rn(__fadd_rn(__fadd_rn(__fsub_rn(z[0][2], z[0][0]),
                                                    __fmul_rn(2.0f, __fsub_rn(z[1][2], z[1][0]))),
                                          __fsub_rn(z[2][2], z[2][0])), 0.125f);
@@ -294,7 +303,7 @@ PM_DEVINL float3 sobel_normal(const float z[3][3], float u, float v, const AdfPa
                                                    __fmul_rn(2.0f, __fsub_rn(z[2][1], z[0][1]))),
                                          __fsub_rn(z[2][2], z[0][2])), 0.125f);
     float mx, my, mz;
-    if (p.nmode == PM_NORMALS_AS_PRINTED) {      // Eq. 2 literally: -K^-1 [Gx, Gy, 1]^T (NEXT-1)
+    if (nmode == PM_NORMALS_AS_PRINTED) {        // Eq. 2 literally: -K^-1 [Gx, Gy, 1]^T (NEXT-1)
         mx = -__fmul_rn(__fsub_rn(gx, p.cx), p.ifx);
         my = -__fmul_rn(__fsub_rn(gy, p.cy), p.ify);
         mz = -1.0f;
@@ -305,7 +314,8 @@ PM_DEVINL float3 sobel_normal(const float z[3][3], float u, float v, const AdfPa
     }
     const float ss = __fmaf_rn(mx, mx, __fmaf_rn(my, my, __fmul_rn(mz, mz)));
     if (!(ss > 0.0f) || !(ss <= FLT_MAX)) return make_float3(0.f, 0.f, 0.f);
-    const float inv = rsqrtf(ss);
+    float inv;                                   // MUFU.RSQ (ss < 2^-126 would flush: |m| >= ~|Z| here)
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(inv) : "f"(ss));
     return make_float3(__fmul_rn(mx, inv), __fmul_rn(my, inv), __fmul_rn(mz, inv));
 }
 
@@ -406,6 +416,8 @@ adf_pass_kernel(const float* __restrict__ src, float* __restrict__ dst, float* _
     float* nrm = normals ? normals + frame * 3 * HW : nullptr;
     if ((W & 3) == 0) {
         constexpr int QW = TW / 4;
+        // CK: window validity checks (tiles with holes); NMC: normals mode
+        auto quads = [&](auto CK, auto NMC) {
         for (int y = warp; y < kTH; y += kWarps) {
             const int gy = oy + y;
             if (gy >= H) break;
@@ -435,7 +447,8 @@ adf_pass_kernel(const float* __restrict__ src, float* __restrict__ dst, float* _
                     const float w3[3][3] = {{z[0][j], z[0][j + 1], z[0][j + 2]},
                                             {z[1][j], z[1][j + 1], z[1][j + 2]},
                                             {z[2][j], z[2][j + 1], z[2][j + 2]}};
-                    const float3 n = sobel_normal(w3, (float)(gx + j), (float)gy, p);
+                    const float3 n = sobel_normal<decltype(CK)::value, decltype(NMC)::value>(
+                        w3, (float)(gx + j), (float)gy, p);
                     px[j] = n.x; py[j] = n.y; pz[j] = n.z;
                 }
                 *reinterpret_cast<float4*>(nrm + o) = nx;
@@ -443,6 +456,17 @@ adf_pass_kernel(const float* __restrict__ src, float* __restrict__ dst, float* _
                 *reinterpret_cast<float4*>(nrm + 2 * HW + o) = nz;
             }
         }
+        };
+        using T_ = std::true_type;
+        using F_ = std::false_type;
+        using GEO = std::integral_constant<int, PM_NORMALS_GEOMETRIC>;
+        using PRN = std::integral_constant<int, PM_NORMALS_AS_PRINTED>;
+        // hole-free tile: every window is valid (lambda <= 1/4 keeps each
+        // update a convex combination of positive depths, so none turns invalid)
+        const bool nocheck = all_valid && p.lam <= 0.25f;
+        if (!nrm) quads(F_{}, GEO{});
+        else if (p.nmode == PM_NORMALS_AS_PRINTED) { if (nocheck) quads(F_{}, PRN{}); else quads(T_{}, PRN{}); }
+        else { if (nocheck) quads(F_{}, GEO{}); else quads(T_{}, GEO{}); }
         return;
     }
     for (int y = warp; y < kTH; y += kWarps) {
