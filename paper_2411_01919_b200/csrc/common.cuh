@@ -82,8 +82,11 @@ struct __align__(8) PackedPoint { uint32_t uv; float z; };
 
 // Deprojection in the exact f32 order of DESIGN.md §3 (Alg. 2 ℓ3):
 // X = (((float)u - cx) * ifx) * z.  Explicit _rn intrinsics: never contracted.
+// Exact u16 -> f32 without the XU pipe: 2^23 + k has k in its low mantissa bits.
+PM_DEVINL float u16_to_f32(uint32_t k) { return __fsub_rn(__uint_as_float(0x4B000000u | k), 8388608.0f); }
+
 PM_DEVINL float3 deproject(PackedPoint p, float cx, float cy, float ifx, float ify) {
-    const float u = (float)(p.uv & 0xFFFFu), v = (float)(p.uv >> 16);
+    const float u = u16_to_f32(p.uv & 0xFFFFu), v = u16_to_f32(p.uv >> 16);
     float3 P;
     P.x = __fmul_rn(__fmul_rn(__fsub_rn(u, cx), ifx), p.z);
     P.y = __fmul_rn(__fmul_rn(__fsub_rn(v, cy), ify), p.z);
@@ -110,6 +113,10 @@ PM_DEVINL void mbar_init(uint64_t* bar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
+
+// Order this CTA's earlier generic-proxy shared-memory accesses (made visible
+// to the issuing thread by a barrier) before a following async-proxy (TMA) write.
+PM_DEVINL void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
 PM_DEVINL void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)

@@ -39,6 +39,7 @@ constexpr int kScoreThreads = 256;
 constexpr int kScoreChunk = 4096;     // points per scoring CTA (dynamic shared memory)
 constexpr int kHB = 8;                // hypothesis array padding
 constexpr int kRefitChunk = 8192;     // points per refit CTA
+constexpr int kRefitWarps = kScoreThreads / 32;   // refit moment slots per (chunk + region)
 
 struct SampleIdx { uint32_t i0, i1, i2; bool ok; };
 
@@ -399,7 +400,6 @@ ransac_select_kernel(RansacWorkspace ws, RansacArgs a) {
 // arithmetic, accumulate fp64 moments, write slot (chunk + region).
 __global__ void __launch_bounds__(kScoreThreads)
 ransac_refit_kernel(RansacWorkspace ws, RansacArgs a) {
-    __shared__ Sums s_part[kScoreThreads / 32];
     __shared__ int s_r0;
     const size_t f = blockIdx.y;
     const int R = ws.R, HP = ws.n_hyp_pad;
@@ -430,15 +430,16 @@ ransac_refit_kernel(RansacWorkspace ws, RansacArgs a) {
             const float3 o3 = deproject(PackedPoint{q0.x, __uint_as_float(q0.y)}, a.K.cx, a.K.cy, ifx, ify);
             const double ox = o3.x, oy = o3.y, oz = o3.z;
             Sums acc = {};
-            for (int i0 = lo + threadIdx.x; i0 < hi; i0 += 4 * kScoreThreads) {
-                uint2 qs[4];
+            constexpr int kU = 8;                             // loads in flight per thread
+            for (int i0 = lo + threadIdx.x; i0 < hi; i0 += kU * kScoreThreads) {
+                uint2 qs[kU];
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {                 // 4 loads in flight per thread
+                for (int u = 0; u < kU; ++u) {
                     const int i = i0 + u * kScoreThreads;
-                    qs[u] = i < hi ? pts[i] : make_uint2(0u, 0u);
+                    qs[u] = i < hi ? __ldg(pts + i) : make_uint2(0u, 0u);
                 }
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
+                for (int u = 0; u < kU; ++u) {
                     if (i0 + u * kScoreThreads >= hi) break;
                     const float3 P = deproject(PackedPoint{qs[u].x, __uint_as_float(qs[u].y)}, a.K.cx, a.K.cy, ifx, ify);
                     const float dist = plane_dist(pl, P);
@@ -452,17 +453,12 @@ ransac_refit_kernel(RansacWorkspace ws, RansacArgs a) {
                     }
                 }
             }
+            // one slot per (chunk + region, warp): no block barrier; the
+            // finalize kernel sums them in (chunk, warp) order (deterministic)
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) sums_add(acc, sums_shfl_xor(acc, o));
-            if (lane == 0) s_part[w] = acc;
-            __syncthreads();
-            if (threadIdx.x == 0) {
-                Sums t = s_part[0];
-                for (int k = 1; k < kScoreThreads / 32; ++k) sums_add(t, s_part[k]);
-                ws.slots[f * (size_t)ws.n_slots + blockIdx.x + r] = t;
-            }
+            if (lane == 0) ws.slots[(f * (size_t)ws.n_slots + blockIdx.x + r) * kRefitWarps + w] = acc;
         }
-        __syncthreads();
     }
 }
 
@@ -535,9 +531,11 @@ ransac_finalize_kernel(RansacWorkspace ws, RansacArgs a, pm_plane* __restrict__ 
     const float4 pl = ws.planes[(f * R + r) * HP + best];
     // slots of this region: chunks c0..c1 -> slot c + r (ascending order)
     const int c0 = base / kRefitChunk, c1 = (base + n - 1) / kRefitChunk;
-    const Sums* sl = ws.slots + f * (size_t)ws.n_slots;
-    Sums t = sl[c0 + r];
-    for (int c = c0 + 1; c <= c1; ++c) sums_add(t, sl[c + r]);
+    const Sums* sl = ws.slots + f * (size_t)ws.n_slots * kRefitWarps;
+    Sums t = sl[(c0 + r) * kRefitWarps];
+    for (int k = 1; k < kRefitWarps; ++k) sums_add(t, sl[(c0 + r) * kRefitWarps + k]);
+    for (int c = c0 + 1; c <= c1; ++c)
+        for (int k = 0; k < kRefitWarps; ++k) sums_add(t, sl[(c + r) * kRefitWarps + k]);
     const uint2* pts = ws.points + f * (size_t)ws.W * ws.H + base;
     const float ifx = 1.0f / a.K.fx, ify = 1.0f / a.K.fy;
     const uint2 q0 = pts[0];
@@ -626,7 +624,7 @@ RansacWorkspace ransac_workspace_layout(void* base, int W, int H, int R, int n_h
     ws.pairs = (float2*)take(sizeof(float4) * B * Rm * (size_t)ws.score_K * ws.score_L);
     ws.counts = (int32_t*)take(sizeof(int32_t) * B * Rm * ws.n_hyp_pad);
     ws.errq = (uint64_t*)take(sizeof(uint64_t) * B * Rm * ws.n_hyp_pad);
-    ws.slots = (Sums*)take(sizeof(Sums) * B * (size_t)ws.n_slots);
+    ws.slots = (Sums*)take(sizeof(Sums) * B * (size_t)ws.n_slots * kRefitWarps);
     ws.best = (int32_t*)take(sizeof(int32_t) * B * Rm);
     ws.total_bytes = o;
     return ws;
