@@ -17,7 +17,10 @@ from typing import NamedTuple
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libpmap.so")
+# PMAP_LIB_VARIANT=<name> loads libpmap_<name>.so from the same directory
+# (A/B kernel timing in tools/ only; default: the in-tree libpmap.so)
+_VARIANT = os.environ.get("PMAP_LIB_VARIANT", "")
+LIB_PATH = os.path.join(_HERE, f"libpmap_{_VARIANT}.so" if _VARIANT else "libpmap.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is missing: build it with `make` (or __graft_entry__.build()); "
