@@ -242,6 +242,8 @@ def run_cuda(args, rank, world, local_rank):
         for _ in range(args.steps):
             step()
         ev1.record(stream)
+        while not ev1.query():           # poll (GIL released) so the sampler thread keeps sampling
+            time.sleep(0.0005)
         torch.cuda.synchronize(dev)
     sys.setswitchinterval(old_switch)
     barrier()

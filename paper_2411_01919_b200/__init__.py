@@ -238,7 +238,9 @@ def ransac_planes(depth: torch.Tensor, K, labels: torch.Tensor, n_regions: int, 
                   select: int = SELECT_COUNT, debug: bool = False, out: torch.Tensor = None,
                   workspace: torch.Tensor = None):
     """Alg. 2 over every region of every frame.  Returns Planes
-    (and, with debug=True, per-hypothesis counts / errq tensors [.., R, n_hyp])."""
+    (and, with debug=True, per-hypothesis counts / errq tensors [.., R, n_hyp];
+    debug="counts": counts only, errq None -- the scoring kernel without the
+    error sums, i.e. the one the default call runs)."""
     B, H, W = _frames(depth, torch.float32)
     if tuple(labels.shape) != tuple(depth.shape):
         raise PMError("pmap: labels must have the depth's shape")
@@ -250,9 +252,10 @@ def ransac_planes(depth: torch.Tensor, K, labels: torch.Tensor, n_regions: int, 
     counts = errq = None
     if debug:
         counts = torch.empty(lead + (n_regions, n_hyp), dtype=torch.int32, device=depth.device)
+    if debug and debug != "counts":   # "counts": counts only (keeps the default scoring kernel)
         errq = torch.empty(lead + (n_regions, n_hyp), dtype=torch.int64, device=depth.device)
-    opt = pm_ransac_options(int(sampler), int(select), counts.data_ptr() if debug else None,
-                            errq.data_ptr() if debug else None)
+    opt = pm_ransac_options(int(sampler), int(select), counts.data_ptr() if counts is not None else None,
+                            errq.data_ptr() if errq is not None else None)
     _check(_lib.pm_ransac_planes_ex(depth.data_ptr(), W, H, B, int(first_frame_id), ctypes.byref(_K(K)),
                                     labels.data_ptr(), int(n_regions), int(n_hyp), float(tau),
                                     int(seed) & (2**64 - 1), out.data_ptr(), ws.data_ptr(), ws.numel(),

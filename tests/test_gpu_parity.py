@@ -156,6 +156,26 @@ def test_ransac_bit_exact(pm, name, kw, filtered):
                     fr["seed"])
 
 
+@pytest.mark.parametrize("n_hyp", [1, 3, 8, 16, 33, 64, 100, 129, 256, 700, 2100])
+def test_ransac_counts_default_kernel_every_layout(pm, n_hyp):
+    """Counts of the default scoring kernel (no error sums: packed FFMA2 pairs
+    for even K) bit-exact against the oracle for every (K, L) layout the
+    launcher picks (n_hyp 1..2100 -> K in {1, 2, 4, 8, 16}, L in 8..256)."""
+    fr = scenegen.make_config("C2", W=200, H=150)
+    d, lab = fr["depth"].numpy(), fr["labels"].numpy()
+    R = 6
+    lab = np.where(lab >= 0, lab % R, -1).astype(np.int32)
+    planes, counts, errq = pm.ransac_planes(torch.from_numpy(d).to(DEV), fr["K"], torch.from_numpy(lab).to(DEV), R,
+                                            n_hyp, fr["tau"], 5, debug="counts")
+    torch.cuda.synchronize()
+    assert errq is None
+    ref = oracle.ransac(d, lab, fr["K"], R, n_hyp, fr["tau"], 5, debug=True)
+    assert np.array_equal(counts.cpu().numpy(), ref["counts"])
+    assert np.array_equal(planes.best_hyp.cpu().numpy(), ref["best_hyp"])
+    assert np.array_equal(planes.inliers.cpu().numpy(), ref["inliers"])
+    assert np.array_equal(planes.status.cpu().numpy(), ref["status"])
+
+
 def test_ransac_noise_free_plane(pm):
     fr = scenegen.make_config("RAMP")
     lab = np.where(fr["depth"].numpy() > 0, 0, -1).astype(np.int32)
