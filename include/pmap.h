@@ -257,19 +257,20 @@ PM_API size_t pm_segment_workspace_bytes(int32_t W, int32_t H, int32_t n_frames,
  * tables (and, if the pointers are not NULL, the filtered depth [B][H][W] and
  * normals [B][3][H][W]) copied back, double-buffered so that the copies of
  * one chunk overlap the kernels of the previous one (the caller's stream plus
- * one internal copy stream per device, created on first use).  Host buffers
+ * two internal copy streams per device -- upload, download -- created on first use).  Host buffers
  * should be pinned (cudaHostAlloc / cudaHostRegister) for the copies to be
  * asynchronous.  Synchronises before returning.
  *   depth_host   [B][H][W] in depth_format: PM_DEPTH_F32_M (f32 metres) or
  *                PM_DEPTH_U16_MM (uint16 millimetres, the sensor's native
  *                format; 0 = invalid; converted as (float)mm * 1e-3f)
- *   labels_host  [B][H][W] in label_format: PM_LABELS_I32 (int32, -1 = none) or
- *                PM_LABELS_U16 (uint16, 0xFFFF = none; n_regions <= 65535)
+ *   labels_host  [B][H][W] in label_format: PM_LABELS_I32 (int32, -1 = none),
+ *                PM_LABELS_U16 (uint16, 0xFFFF = none; n_regions <= 65535) or
+ *                PM_LABELS_U8 (uint8, 0xFF = none; n_regions <= 255)
  *   planes_host  [B][n_regions] pm_plane (host)
  *   arena        device memory >= pm_host_pipeline_arena_bytes(...), 256-B aligned.
  * Other arguments as pm_process_frames. */
 enum { PM_DEPTH_F32_M = 0, PM_DEPTH_U16_MM = 1 };
-enum { PM_LABELS_I32 = 0, PM_LABELS_U16 = 1 };
+enum { PM_LABELS_I32 = 0, PM_LABELS_U16 = 1, PM_LABELS_U8 = 2 };
 PM_API pm_status pm_process_frames_host(const void* depth_host, int32_t depth_format, const void* labels_host,
                                         int32_t label_format, int32_t W, int32_t H, int32_t n_frames,
                                         uint32_t first_frame_id, const pm_intrinsics* K, float lambda,

@@ -35,7 +35,7 @@ ADF_ALG1, ADF_DIVERGENCE = 0, 1
 NORMALS_GEOMETRIC, NORMALS_AS_PRINTED = 0, 1
 ENGINE_AUTO, ENGINE_TILED, ENGINE_STREAM = 0, 1, 2
 DEPTH_F32_M, DEPTH_U16_MM = 0, 1
-LABELS_I32, LABELS_U16 = 0, 1
+LABELS_I32, LABELS_U16, LABELS_U8 = 0, 1, 2
 PLANE_WORDS = 12          # sizeof(pm_plane) / 4
 
 
@@ -314,9 +314,9 @@ def process_frames_host(depth: torch.Tensor, labels: torch.Tensor, K, lam: float
     if depth.dim() != 3 or tuple(labels.shape) != tuple(depth.shape):
         raise PMError("pmap: expected [B, H, W] depth and labels")
     dfmt = {torch.float32: DEPTH_F32_M, torch.uint16: DEPTH_U16_MM}.get(depth.dtype)
-    lfmt = {torch.int32: LABELS_I32, torch.uint16: LABELS_U16}.get(labels.dtype)
+    lfmt = {torch.int32: LABELS_I32, torch.uint16: LABELS_U16, torch.uint8: LABELS_U8}.get(labels.dtype)
     if dfmt is None or lfmt is None or not depth.is_contiguous() or not labels.is_contiguous():
-        raise PMError("pmap: depth float32|uint16, labels int32|uint16, contiguous")
+        raise PMError("pmap: depth float32|uint16, labels int32|uint16|uint8, contiguous")
     B, H, W = depth.shape
     dev = torch.device("cuda") if device is None else torch.device(device)
     C = min(int(chunk_frames), B)

@@ -1,8 +1,10 @@
 // host_pipeline.cu — the whole path for frames in HOST memory
 // (pm_process_frames_host): chunked, double-buffered H2D / compute / D2H on
-// the caller's stream plus one internal copy stream per device, so the copy
-// of chunk k+1 overlaps the kernels of chunk k.  Sensor-native inputs
-// (uint16 millimetres; uint16 labels) halve the PCIe bytes.
+// the caller's stream plus two internal copy streams per device (one per
+// direction: a D2H waiting for chunk k's kernels must not hold back the H2D
+// of chunk k+1), so the upload of chunk k+1 overlaps the kernels of chunk k
+// and the link stays busy.  Sensor-native inputs (uint16 millimetres,
+// S:26-28; uint16 / uint8 labels) cut the PCIe bytes.
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <string.h>
@@ -40,8 +42,16 @@ u16_labels_kernel(const uint16_t* __restrict__ in, int32_t* __restrict__ out, si
     if (i < n) out[i] = in[i] == 0xFFFFu ? -1 : (int32_t)in[i];
 }
 
+// uint8 labels -> int32, 0xFF -> -1 (unlabelled)
+__global__ void __launch_bounds__(kConvThreads)
+u8_labels_kernel(const uint8_t* __restrict__ in, int32_t* __restrict__ out, size_t n) {
+    const size_t i = (size_t)blockIdx.x * kConvThreads + threadIdx.x;
+    if (i < n) out[i] = in[i] == 0xFFu ? -1 : (int32_t)in[i];
+}
+
 struct DeviceStreams {
-    cudaStream_t copy = nullptr;
+    cudaStream_t copy = nullptr;      // H2D
+    cudaStream_t down = nullptr;      // D2H
     cudaEvent_t h2d[2] = {}, done[2] = {}, freed[2] = {};
     std::mutex mu;            // one host pipeline at a time per device
     cudaError_t err = cudaSuccess;
@@ -56,6 +66,7 @@ DeviceStreams* streams_for_current_device() {
     if (!per_dev[dev]) {
         DeviceStreams* d = new DeviceStreams();
         d->err = cudaStreamCreateWithFlags(&d->copy, cudaStreamNonBlocking);
+        if (d->err == cudaSuccess) d->err = cudaStreamCreateWithFlags(&d->down, cudaStreamNonBlocking);
         for (int s = 0; s < 2 && d->err == cudaSuccess; ++s) {
             d->err = cudaEventCreateWithFlags(&d->h2d[s], cudaEventDisableTiming);
             if (d->err == cudaSuccess) d->err = cudaEventCreateWithFlags(&d->done[s], cudaEventDisableTiming);
@@ -97,7 +108,9 @@ Arena arena_layout(void* base, int W, int H, int R, int n_hyp, int C, int depth_
         sl.depth = (float*)take(sizeof(float) * px);
         sl.raw_depth = depth_fmt == PM_DEPTH_U16_MM ? take(sizeof(uint16_t) * px) : (void*)sl.depth;
         sl.labels = (int32_t*)take(sizeof(int32_t) * px);
-        sl.raw_labels = label_fmt == PM_LABELS_U16 ? take(sizeof(uint16_t) * px) : (void*)sl.labels;
+        sl.raw_labels = label_fmt == PM_LABELS_U16 ? take(sizeof(uint16_t) * px)
+                        : label_fmt == PM_LABELS_U8 ? take(sizeof(uint8_t) * px)
+                                                    : (void*)sl.labels;
         sl.depth_out = (float*)take(sizeof(float) * px);
         sl.normals = (float*)take(sizeof(float) * 3 * px);
         sl.planes = (pm_plane*)take(sizeof(pm_plane) * (size_t)C * (R > 0 ? R : 1));
@@ -142,8 +155,10 @@ PM_API pm_status pm_process_frames_host(const void* depth_host, int32_t depth_fo
     if (!depth_host || !labels_host || !planes_host || chunk_frames < 1 || n_frames < 1)
         return PM_ERR_INVALID_ARGUMENT;
     if (depth_format != PM_DEPTH_F32_M && depth_format != PM_DEPTH_U16_MM) return PM_ERR_INVALID_ARGUMENT;
-    if (label_format != PM_LABELS_I32 && label_format != PM_LABELS_U16) return PM_ERR_INVALID_ARGUMENT;
+    if (label_format != PM_LABELS_I32 && label_format != PM_LABELS_U16 && label_format != PM_LABELS_U8)
+        return PM_ERR_INVALID_ARGUMENT;
     if (label_format == PM_LABELS_U16 && n_regions > 65535) return PM_ERR_INVALID_ARGUMENT;
+    if (label_format == PM_LABELS_U8 && n_regions > 255) return PM_ERR_INVALID_ARGUMENT;
     const int C = chunk_frames < n_frames ? chunk_frames : n_frames;
     if (!arena || arena_bytes < pm_host_pipeline_arena_bytes(W, H, n_regions, n_hyp, C, depth_format, label_format) ||
         ((uintptr_t)arena & 255u))
@@ -155,7 +170,7 @@ PM_API pm_status pm_process_frames_host(const void* depth_host, int32_t depth_fo
     cudaStream_t cs = (cudaStream_t)stream;
     const size_t frame_px = (size_t)W * H;
     const size_t dsz = depth_format == PM_DEPTH_U16_MM ? 2 : 4;
-    const size_t lsz = label_format == PM_LABELS_U16 ? 2 : 4;
+    const size_t lsz = label_format == PM_LABELS_U16 ? 2 : label_format == PM_LABELS_U8 ? 1 : 4;
     const int n_chunks = (n_frames + C - 1) / C;
     cudaError_t e = cudaSuccess;
     // both slots start free
@@ -186,26 +201,31 @@ PM_API pm_status pm_process_frames_host(const void* depth_host, int32_t depth_fo
             u16_labels_kernel<<<(unsigned)((px + kConvThreads - 1) / kConvThreads), kConvThreads, 0, cs>>>(
                 (const uint16_t*)sl.raw_labels, sl.labels, px);
             if ((e = cudaGetLastError()) != cudaSuccess) break;
+        } else if (label_format == PM_LABELS_U8) {
+            u8_labels_kernel<<<(unsigned)((px + kConvThreads - 1) / kConvThreads), kConvThreads, 0, cs>>>(
+                (const uint8_t*)sl.raw_labels, sl.labels, px);
+            if ((e = cudaGetLastError()) != cudaSuccess) break;
         }
         pm_status st = pm_process_frames(sl.depth, sl.labels, W, H, nf, first_frame_id + (uint32_t)f0, K, lambda,
                                          kappa, iters, n_regions, n_hyp, inlier_thresh, seed, sl.depth_out,
                                          sl.normals, sl.planes, sl.ws, sl.ws_bytes, stream);
         if (st != PM_OK) return st;
         e = cudaEventRecord(ds->done[s], cs);
-        // D2H of the results on the copy stream; the slot is free afterwards
-        if (e == cudaSuccess) e = cudaStreamWaitEvent(ds->copy, ds->done[s], 0);
+        // D2H of the results on the download stream; the slot is free afterwards
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(ds->down, ds->done[s], 0);
         if (e == cudaSuccess && n_regions > 0)
             e = cudaMemcpyAsync(planes_host + (size_t)f0 * n_regions, sl.planes, sizeof(pm_plane) * nf * n_regions,
-                                cudaMemcpyDeviceToHost, ds->copy);
+                                cudaMemcpyDeviceToHost, ds->down);
         if (e == cudaSuccess && depth_out_host)
             e = cudaMemcpyAsync(depth_out_host + (size_t)f0 * frame_px, sl.depth_out, sizeof(float) * px,
-                                cudaMemcpyDeviceToHost, ds->copy);
+                                cudaMemcpyDeviceToHost, ds->down);
         if (e == cudaSuccess && normals_host)
             e = cudaMemcpyAsync(normals_host + (size_t)f0 * 3 * frame_px, sl.normals, sizeof(float) * 3 * px,
-                                cudaMemcpyDeviceToHost, ds->copy);
-        if (e == cudaSuccess) e = cudaEventRecord(ds->freed[s], ds->copy);
+                                cudaMemcpyDeviceToHost, ds->down);
+        if (e == cudaSuccess) e = cudaEventRecord(ds->freed[s], ds->down);
     }
     if (e == cudaSuccess) e = cudaStreamSynchronize(ds->copy);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ds->down);
     if (e == cudaSuccess) e = cudaStreamSynchronize(cs);
     return e == cudaSuccess ? PM_OK : PM_ERR_CUDA;
 }

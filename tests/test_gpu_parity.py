@@ -351,6 +351,11 @@ def test_host_pipeline_matches_device_pipeline(pm):
     planes_f = pm.process_frames_host(dm.cpu().contiguous(), lab.contiguous(), K, 0.15, 0.03, 20, R, NH, 0.01, 77,
                                       first_frame_id=100, chunk_frames=8)
     assert torch.equal(planes_f.raw, planes_d.raw.cpu())
+    # uint8 labels (0xFF = none), three chunks of 2 + 2 + 1 frames
+    lab8 = torch.where(lab < 0, torch.full_like(lab, 0xFF), lab).to(torch.uint8)
+    planes_8 = pm.process_frames_host(mm.pin_memory(), lab8.pin_memory(), K, 0.15, 0.03, 20, R, NH, 0.01, 77,
+                                      first_frame_id=100, chunk_frames=2)
+    assert torch.equal(planes_8.raw, planes_d.raw.cpu())
     # and against the oracle for one frame
     ref = oracle.ransac(d_dev[3].cpu().numpy(), lab[3].numpy(), K, R, NH, 0.01, 77, frame_id=103)
     assert np.array_equal(planes_h.best_hyp[3].numpy(), ref["best_hyp"])
