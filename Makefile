@@ -2,7 +2,8 @@
 NVCC     ?= /usr/local/cuda/bin/nvcc
 PKG      := paper_2411_01919_b200
 SRC      := $(wildcard $(PKG)/csrc/*.cu)
-OBJ      := $(patsubst $(PKG)/csrc/%.cu,build/%.o,$(SRC))
+CPPSRC   := $(wildcard $(PKG)/csrc/*.cpp)
+OBJ      := $(patsubst $(PKG)/csrc/%.cu,build/%.o,$(SRC)) $(patsubst $(PKG)/csrc/%.cpp,build/%.cpp.o,$(CPPSRC))
 HDR      := $(wildcard $(PKG)/csrc/*.cuh $(PKG)/csrc/*.h) include/pmap.h
 LIB      := $(PKG)/libpmap.so
 # --fmad=false: no implicit FMA contraction; every fused multiply-add the
@@ -15,6 +16,11 @@ all: $(LIB) oracle/liboracle.so
 build/%.o: $(PKG)/csrc/%.cu $(HDR)
 	@mkdir -p build
 	$(NVCC) $(NVFLAGS) -c -o $@ $<
+
+# host-only C++ (NEXT-4 map manager)
+build/%.cpp.o: $(PKG)/csrc/%.cpp $(HDR)
+	@mkdir -p build
+	g++ -O2 -std=c++17 -fPIC -fvisibility=hidden -Iinclude -c -o $@ $<
 
 $(LIB): $(OBJ)
 	$(NVCC) -shared -gencode arch=compute_100a,code=sm_100a -o $@.tmp $(OBJ) && mv $@.tmp $@

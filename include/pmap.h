@@ -284,6 +284,59 @@ PM_API size_t pm_host_pipeline_arena_bytes(int32_t W, int32_t H, int32_t n_regio
 PM_API pm_status pm_depth_u16_to_metres(const uint16_t* depth_mm, float* depth_m, size_t n, float scale,
                                         pm_stream_t stream);
 
+/* ---------------------------------------------------------------------- */
+/* NEXT-4 of SURVEY §8(f), HOST code (no device work): the paper's map merge
+ * gate and vertical-drift Kalman filter (§III-E) applied to the
+ * plane table (one plane per region in place of the paper's polygon;
+ * DESIGN.md readings Q30-Q34).  All in fp64. */
+typedef struct {
+    double x;      /* drift estimate x_k|k (metres, world z) */
+    double P;      /* its covariance P_k|k */
+} pm_drift_filter;
+
+/* Eqs. 6-10 in order: x_pred = x (6); P_pred = P + sigma_p (7);
+ * K = P_pred / (P_pred + sigma_m) (8); x = x_pred + K (z - x_pred) (9);
+ * P = (1 - K) P_pred (10).  Updates *f, returns K (NaN if f is NULL). */
+PM_API double pm_drift_kalman_step(pm_drift_filter* f, double z, double sigma_p, double sigma_m);
+
+/* Eqs. 4-5: dz = |z_new - z_map| (written to *dz_out if not
+ * NULL); returns 1 iff dz <= drift_tol ("merge"), else 0. */
+PM_API int32_t pm_merge_gate(double z_new, double z_map, double drift_tol, double* dz_out);
+
+typedef struct {
+    double n[3];   /* unit normal, world frame */
+    double c[3];   /* centroid, world frame (drift-compensated z) */
+    double w;      /* merge weight: accumulated inlier count */
+    int32_t n_obs; /* observations merged into this plane */
+    int32_t pad;
+} pm_map_plane;
+
+typedef struct {
+    double drift_tol;   /* Eq. 5 tolerance (paper: 0.05 m) */
+    double normal_tol;  /* max angle between normals to match (rad) */
+    double xy_radius;   /* max horizontal centroid distance to match (m) */
+    double sigma_p;     /* Eq. 7 process noise */
+    double sigma_m;     /* Eq. 8 measurement noise */
+} pm_map_params;
+
+/* One frame's plane table into the map (Q31-Q34): PM_PLANE_OK
+ * planes to the world frame with `pose` (row-major 4x4 camera-to-world),
+ * z minus the drift estimate; each is matched to the map plane (as it was
+ * before this frame) that passes the gate -- normals within normal_tol,
+ * horizontal centroid distance <= xy_radius, Eq. 5 on the centroid heights --
+ * with the smallest horizontal distance (ties: lowest index); if any matched,
+ * z_k = mean signed (z_new - z_map) + x and one Kalman step (Eqs. 6-10), the
+ * incoming heights re-adjusted by the change of x; matched planes are merged
+ * (inlier-weighted normal and centroid), the others appended in frame order.
+ *   map          [map_capacity] pm_map_plane, *map_count in use (in/out)
+ *   match_out    [n_planes] matched map index or -1 (inserted / not OK), nullable
+ *   z_k_out      the drift measurement, NaN when nothing matched, nullable
+ * Returns PM_ERR_WORKSPACE (map untouched) if the inserts exceed capacity. */
+PM_API pm_status pm_plane_map_merge_frame(pm_map_plane* map, int32_t* map_count, int32_t map_capacity,
+                                          const pm_plane* frame, int32_t n_planes, const double pose[16],
+                                          pm_drift_filter* filter, const pm_map_params* prm,
+                                          int32_t* match_out, double* z_k_out);
+
 /* Number of kernel launches one pm_process_frames call enqueues (for the
  * bench's launch accounting; memsets excluded). */
 PM_API int32_t pm_pipeline_kernel_launches(int32_t iters, int32_t n_regions);

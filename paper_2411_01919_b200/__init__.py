@@ -106,6 +106,7 @@ EXPORTED = ("pm_adf_filter", "pm_adf_filter_batched", "pm_adf_filter_ex", "pm_ad
             "pm_process_frames", "pm_pipeline_workspace_bytes", "pm_pipeline_kernel_launches",
             "pm_process_frames_host", "pm_host_pipeline_arena_bytes", "pm_depth_u16_to_metres",
             "pm_segment_regions", "pm_segment_workspace_bytes",
+            "pm_drift_kalman_step", "pm_merge_gate", "pm_plane_map_merge_frame",
             "pm_status_string", "pm_version")
 
 
@@ -364,3 +365,70 @@ def segment_regions(normals: torch.Tensor, canny_low: float = 30.0, canny_high: 
         labels = labels[0]
         emask = emask[0] if edges else None
     return labels, nreg, emask
+
+
+# ---------------------------------------------------------------- NEXT-4 (host)
+class pm_drift_filter(ctypes.Structure):
+    _fields_ = [("x", ctypes.c_double), ("P", ctypes.c_double)]
+
+
+class pm_map_plane(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_double * 3), ("c", ctypes.c_double * 3), ("w", ctypes.c_double),
+                ("n_obs", ctypes.c_int32), ("pad", ctypes.c_int32)]
+
+
+class pm_map_params(ctypes.Structure):
+    _fields_ = [("drift_tol", ctypes.c_double), ("normal_tol", ctypes.c_double), ("xy_radius", ctypes.c_double),
+                ("sigma_p", ctypes.c_double), ("sigma_m", ctypes.c_double)]
+
+
+_lib.pm_drift_kalman_step.restype = ctypes.c_double
+_lib.pm_drift_kalman_step.argtypes = [ctypes.POINTER(pm_drift_filter), ctypes.c_double, ctypes.c_double,
+                                      ctypes.c_double]
+_lib.pm_merge_gate.restype = _I32
+_lib.pm_merge_gate.argtypes = [ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.POINTER(ctypes.c_double)]
+_lib.pm_plane_map_merge_frame.restype = ctypes.c_int
+
+
+def drift_kalman_step(f: pm_drift_filter, z: float, sigma_p: float, sigma_m: float) -> float:
+    """Eqs. 6-10 on the host; updates f, returns the gain K."""
+    return float(_lib.pm_drift_kalman_step(ctypes.byref(f), float(z), float(sigma_p), float(sigma_m)))
+
+
+def merge_gate(z_new: float, z_map: float, drift_tol: float = 0.05):
+    """Eqs. 4-5 (P:347-353): (dz, merge?)."""
+    dz = ctypes.c_double()
+    ok = _lib.pm_merge_gate(float(z_new), float(z_map), float(drift_tol), ctypes.byref(dz))
+    return dz.value, bool(ok)
+
+
+class PlaneMap:
+    """Host-side plane map with drift compensation (NEXT-4): wraps
+    pm_plane_map_merge_frame over a fixed-capacity pm_map_plane array."""
+
+    def __init__(self, capacity: int = 4096, drift_tol: float = 0.05, normal_tol: float = 0.1745,
+                 xy_radius: float = 0.5, sigma_p: float = 1e-4, sigma_m: float = 1e-4, P0: float = 1.0):
+        self.capacity = int(capacity)
+        self.planes = (pm_map_plane * self.capacity)()
+        self.count = ctypes.c_int32(0)
+        self.filter = pm_drift_filter(0.0, float(P0))
+        self.params = pm_map_params(drift_tol, normal_tol, xy_radius, sigma_p, sigma_m)
+
+    def merge_frame(self, plane_table: torch.Tensor, pose):
+        """plane_table: int32 [R, 12] raw pm_plane rows (Planes.raw of one
+        frame, any device); pose: 16 floats, row-major camera-to-world.
+        Returns (match [R] list, z_k or None)."""
+        raw = plane_table.detach().to("cpu", torch.int32).contiguous()
+        R = raw.shape[0]
+        pose_c = (ctypes.c_double * 16)(*[float(v) for v in pose])
+        match = (ctypes.c_int32 * max(R, 1))()
+        zk = ctypes.c_double()
+        _check(_lib.pm_plane_map_merge_frame(self.planes, ctypes.byref(self.count), self.capacity,
+                                             ctypes.c_void_p(raw.data_ptr()), R, pose_c, ctypes.byref(self.filter),
+                                             ctypes.byref(self.params), match, ctypes.byref(zk)))
+        z = zk.value
+        return list(match)[:R], (None if z != z else z)
+
+    def as_list(self):
+        return [{"n": list(p.n), "c": list(p.c), "w": p.w, "n_obs": p.n_obs}
+                for p in self.planes[:self.count.value]]
