@@ -73,6 +73,11 @@ def lib() -> ctypes.CDLL:
             L.orc_normals_to_u8.restype = None
             L.orc_canny_u8.argtypes = [P, i32, i32, i32, f64, f64, P]
             L.orc_segment_regions.argtypes = [P, i32, i32, f64, f64, i32, i32, P, P, P]
+            L.orc_trace_contour.argtypes = [P, i32, i32, i32, P, i32]
+            L.orc_simplify_dp.argtypes = [P, i32, i32, P]
+            L.orc_rasterize_polygons.argtypes = [P, P, P, i32, i32, i32, P]
+            L.orc_lift_vertices.argtypes = [P, i32, P, f64, f64, f64, f64, P]
+            L.orc_lift_vertices.restype = None
             _lib = L
     return _lib
 
@@ -231,3 +236,51 @@ def segment_regions(normals: np.ndarray, low: float = 30.0, high: float = 90.0, 
     assert lib().orc_segment_regions(_p(n), W, H, float(low), float(high), int(min_area), int(max_regions),
                                      _p(labels), _p(nr), _p(edges)) == 0
     return labels, int(nr[0]), edges
+
+
+# ---------------------------------------------------------------- NEXT-3
+def trace_contour(labels: np.ndarray, region: int) -> np.ndarray:
+    """Q35: outer boundary of `region` by Moore-neighbour tracing: int32 [n, 2] (x, y)."""
+    lab = _c(labels, np.int32)
+    H, W = lab.shape
+    cap = 2 * (W + H) + 4 * int((lab == region).sum()) + 8
+    pts = np.empty((cap, 2), np.int32)
+    n = lib().orc_trace_contour(_p(lab), W, H, int(region), _p(pts), cap)
+    assert n <= cap
+    return pts[:n].copy()
+
+
+def simplify_dp(pts: np.ndarray, eps: float, return_index: bool = False):
+    """Q36: Douglas-Peucker on a closed integer contour [n, 2], eps in px
+    (exact, eps rounded to 1/16 px): the kept points in contour order (and
+    their contour indices)."""
+    a = _c(pts, np.int32)
+    keep = np.zeros(len(a), np.uint8)
+    m = lib().orc_simplify_dp(_p(a), len(a), int(round(eps * 16)), _p(keep))
+    idx = np.nonzero(keep)[0]
+    assert len(idx) == m
+    return (a[idx], idx) if return_index else a[idx]
+
+
+def rasterize_polygons(polys, W: int, H: int) -> np.ndarray:
+    """Q37/Q38: list of int32 [m, 2] vertex arrays -> label image int32 [H, W]."""
+    offs, nv, vs = [], [], []
+    o = 0
+    for q in polys:
+        q = np.asarray(q, np.int32).reshape(-1, 2)
+        offs.append(o); nv.append(len(q)); vs.append(q)
+        o += len(q)
+    verts = np.ascontiguousarray(np.concatenate(vs) if vs else np.zeros((0, 2), np.int32), np.int32)
+    offs = np.asarray(offs, np.int32); nv = np.asarray(nv, np.int32)
+    out = np.empty((H, W), np.int32)
+    assert lib().orc_rasterize_polygons(_p(verts), _p(offs), _p(nv), len(polys), W, H, _p(out)) == 0
+    return out
+
+
+def lift_vertices(uv: np.ndarray, plane, K) -> np.ndarray:
+    """Q39: pixel vertices [n, 2] onto plane (nx, ny, nz, d) along camera rays -> [n, 3] f64."""
+    a = _c(uv, np.int32)
+    pl = np.asarray(plane, np.float64)
+    X = np.empty((len(a), 3), np.float64)
+    lib().orc_lift_vertices(_p(a), len(a), _p(pl), float(K.fx), float(K.fy), float(K.cx), float(K.cy), _p(X))
+    return X

@@ -700,3 +700,171 @@ ORC_API int orc_segment_regions(const float* nrm, int W, int H, double low, doub
     free(img); free(e0); free(e1); free(comp); free(queue); free(seed); free(size); free(order); free(rank);
     return 0;
 }
+
+/* ======================================================================
+ * NEXT-3: polygon glue between region labels and planes
+ * ("contours are extracted from these edges and simplified into
+ * polygons", Alg. 2 "for each detected contour c").
+ * Readings Q35-Q39 in DESIGN.md.
+ * ====================================================================== */
+
+/* Q35: outer boundary of region `region` of a label image by Moore-neighbour
+ * tracing.  Start: the region's first pixel in raster order, backtrack = its
+ * west neighbour.  Neighbours are visited clockwise on screen (x right, y
+ * down) starting just after the backtrack direction: E, SE, S, SW, W, NW, N,
+ * NE.  Pixels outside the image or of another label are background.  Stops
+ * when the walk is back at the start pixel about to repeat its first move
+ * (Jacob's criterion).  Writes up to max_pts (x, y) pairs to pts, returns the
+ * contour length (which may exceed max_pts: the output is then truncated), 0
+ * when the region is empty.                                                  */
+static const int ORC_MOORE[8][2] = {{1, 0}, {1, 1}, {0, 1}, {-1, 1}, {-1, 0}, {-1, -1}, {0, -1}, {1, -1}};
+
+static int orc_in_region(const int32_t* labels, int W, int H, int x, int y, int region)
+{
+    return x >= 0 && y >= 0 && x < W && y < H && labels[(size_t)y * W + x] == region;
+}
+
+ORC_API int orc_trace_contour(const int32_t* labels, int W, int H, int region, int32_t* pts, int max_pts)
+{
+    size_t n = (size_t)W * H, s = n;
+    for (size_t p = 0; p < n; ++p) if (labels[p] == region) { s = p; break; }
+    if (s == n) return 0;
+    int sx = (int)(s % W), sy = (int)(s / W);
+    int len = 0;
+    int px = sx, py = sy, bdir = 4;                  /* backtrack: west */
+    int first_dir = -1;
+    for (;;) {
+        int found = -1;
+        for (int k = 1; k <= 8; ++k) {
+            int d = (bdir + k) & 7;
+            if (orc_in_region(labels, W, H, px + ORC_MOORE[d][0], py + ORC_MOORE[d][1], region)) { found = d; break; }
+        }
+        if (found < 0) {                             /* isolated pixel */
+            if (max_pts > 0) { pts[0] = px; pts[1] = py; }
+            return 1;
+        }
+        if (px == sx && py == sy) {
+            if (first_dir < 0) first_dir = found;
+            else if (found == first_dir) break;      /* Jacob's stopping criterion */
+        }
+        if (len < max_pts) { pts[2 * len] = px; pts[2 * len + 1] = py; }
+        len++;
+        /* move; the new backtrack is the background neighbour examined just
+         * before `found`, seen from the new pixel */
+        int bd = (found + 7) & 7;                    /* previous direction examined (background) */
+        int bx = px + ORC_MOORE[bd][0], by = py + ORC_MOORE[bd][1];
+        px += ORC_MOORE[found][0];
+        py += ORC_MOORE[found][1];
+        int dxb = bx - px, dyb = by - py;
+        for (int d = 0; d < 8; ++d) if (ORC_MOORE[d][0] == dxb && ORC_MOORE[d][1] == dyb) { bdir = d; break; }
+    }
+    return len;
+}
+
+/* Q36: Douglas-Peucker simplification of a closed contour of n integer
+ * points.  Anchors: point 0 and the point farthest from it
+ * (largest squared distance, ties -> lowest index); each open chain i..j is
+ * split at the point k of largest distance to the LINE through p_i, p_j
+ * (to p_i itself when p_i == p_j), ties -> lowest k, if that distance > eps.
+ * Exact: |cross| compared among k, then cross^2 > eps^2 |p_j - p_i|^2 in
+ * 128-bit integers with eps given in 1/16 px (eps16).  keep[n] (0/1) marks
+ * the retained vertices; returns their number.                             */
+static void orc_dp_rec(const int32_t* pts, int n, int i, int j, int64_t eps16, uint8_t* keep)
+{
+    /* chain i, i+1, ..., j (indices mod n) */
+    int cnt = (j - i + n) % n;
+    if (cnt < 2) return;
+    int64_t ax = pts[2 * i], ay = pts[2 * i + 1], bx = pts[2 * (j % n)], by = pts[2 * (j % n) + 1];
+    int64_t dx = bx - ax, dy = by - ay;
+    int best = -1;
+    unsigned __int128 bestv = 0;
+    for (int s = 1; s < cnt; ++s) {
+        int k = (i + s) % n;
+        int64_t px = pts[2 * k] - ax, py = pts[2 * k + 1] - ay;
+        unsigned __int128 v;
+        if (dx == 0 && dy == 0) v = (unsigned __int128)(px * px + py * py);
+        else {
+            int64_t c = dx * py - dy * px;
+            if (c < 0) c = -c;
+            v = (unsigned __int128)c;
+        }
+        if (best < 0 || v > bestv) { best = k; bestv = v; }
+    }
+    /* distance > eps:  point case: d2 > eps^2 ; line case: cross^2 > eps^2 len^2 */
+    unsigned __int128 lhs, rhs;
+    if (dx == 0 && dy == 0) { lhs = bestv * 256u; rhs = (unsigned __int128)(eps16 * eps16); }
+    else {
+        lhs = bestv * bestv * 256u;
+        rhs = (unsigned __int128)(eps16 * eps16) * (unsigned __int128)(dx * dx + dy * dy);
+    }
+    if (lhs > rhs) {
+        keep[best] = 1;
+        orc_dp_rec(pts, n, i, best, eps16, keep);
+        orc_dp_rec(pts, n, best, j, eps16, keep);
+    }
+}
+
+ORC_API int orc_simplify_dp(const int32_t* pts, int n, int eps16, uint8_t* keep)
+{
+    if (n <= 0) return 0;
+    for (int k = 0; k < n; ++k) keep[k] = 0;
+    keep[0] = 1;
+    if (n == 1) return 1;
+    int far = 0;
+    int64_t fd = -1;
+    for (int k = 1; k < n; ++k) {
+        int64_t dx = pts[2 * k] - pts[0], dy = pts[2 * k + 1] - pts[1];
+        int64_t d2 = dx * dx + dy * dy;
+        if (d2 > fd) { fd = d2; far = k; }
+    }
+    keep[far] = 1;
+    orc_dp_rec(pts, n, 0, far, eps16, keep);
+    orc_dp_rec(pts, n, far, n, eps16, keep);   /* far .. n-1, 0 (index n == 0 mod n) */
+    int m = 0;
+    for (int k = 0; k < n; ++k) m += keep[k];
+    return m;
+}
+
+/* Q37/Q38: rasterise polygons (integer vertices = pixel centres) to a label
+ * image: pixel (x, y) is inside polygon q by the even-odd rule on its centre
+ * with half-open crossings -- edge a->b counts iff (a.y > y) != (b.y > y) and
+ * x < a.x + (y - a.y)(b.x - a.x)/(b.y - a.y), evaluated exactly in integers;
+ * a pixel inside several polygons takes the lowest polygon index, -1 when in
+ * none.  Polygon q has n_v[q] vertices at verts + 2*off[q].                 */
+ORC_API int orc_rasterize_polygons(const int32_t* verts, const int32_t* off, const int32_t* n_v, int n_poly,
+                                   int W, int H, int32_t* labels)
+{
+    for (size_t p = 0; p < (size_t)W * H; ++p) labels[p] = -1;
+    for (int y = 0; y < H; ++y)
+        for (int x = 0; x < W; ++x)
+            for (int q = 0; q < n_poly; ++q) {
+                const int32_t* v = verts + 2 * (size_t)off[q];
+                int m = n_v[q], inside = 0;
+                for (int e = 0; e < m; ++e) {
+                    int64_t ax = v[2 * e], ay = v[2 * e + 1];
+                    int64_t bx = v[2 * ((e + 1) % m)], by = v[2 * ((e + 1) % m) + 1];
+                    if ((ay > y) == (by > y)) continue;
+                    /* x < ax + (y - ay)(bx - ax)/(by - ay)  <=>  (x - ax)(by - ay) < (y - ay)(bx - ax) * sign */
+                    int64_t lhs = (x - ax) * (by - ay), rhs = (y - ay) * (bx - ax);
+                    int cross = (by > ay) ? (lhs < rhs) : (lhs > rhs);
+                    if (cross) inside ^= 1;
+                }
+                if (inside) { labels[(size_t)y * W + x] = q; break; }
+            }
+    return 0;
+}
+
+/* Q39: lift pixel vertices onto a plane n.X + d = 0 along their camera rays
+ * (S:327): r = ((u - cx)/fx, (v - cy)/fy, 1), X = -d/(n.r) r in fp64; NaN
+ * when n.r == 0 or the intersection is behind the camera.                   */
+ORC_API void orc_lift_vertices(const int32_t* uv, int n, const double plane[4], double fx, double fy, double cx,
+                               double cy, double* X)
+{
+    for (int k = 0; k < n; ++k) {
+        double r0 = ((double)uv[2 * k] - cx) / fx, r1 = ((double)uv[2 * k + 1] - cy) / fy, r2 = 1.0;
+        double den = plane[0] * r0 + plane[1] * r1 + plane[2] * r2;
+        double t = den != 0.0 ? -plane[3] / den : NAN;
+        if (!(t > 0.0)) { X[3 * k] = X[3 * k + 1] = X[3 * k + 2] = NAN; continue; }
+        X[3 * k] = t * r0; X[3 * k + 1] = t * r1; X[3 * k + 2] = t * r2;
+    }
+}
