@@ -285,6 +285,51 @@ PM_API pm_status pm_depth_u16_to_metres(const uint16_t* depth_mm, float* depth_m
                                         pm_stream_t stream);
 
 /* ---------------------------------------------------------------------- */
+/* NEXT-3 of SURVEY §8(f): polygon glue between region labels and planes
+ * ("contours are extracted from these edges and simplified into
+ * polygons"; readings Q35-Q39 in DESIGN.md).
+ * All buffers device memory, batched over n_frames x n_regions slots. */
+typedef struct {
+    int32_t eps16;         /* Douglas-Peucker tolerance in 1/16 px (S:262 default 3 px = 48) */
+    int32_t max_contour;   /* capacity of a traced contour (points) */
+    int32_t max_vertices;  /* capacity of a simplified polygon (vertices, >= 3) */
+} pm_polygon_params;
+
+/* Per region r of each frame's label image [B][H][W] (int32, r in
+ * [0, n_regions), others ignored): the outer boundary by Moore-neighbour
+ * tracing from the region's first pixel in raster order (clockwise on
+ * screen; Q35), then closed Douglas-Peucker with exact integer distance tests
+ * (anchors: the start and the farthest point; Q36).
+ *   contour_len  [B][R]   traced length (> max_contour: truncated), 0 = empty
+ *   vertices     [B][R][max_vertices][2] int32 (x, y) in contour order
+ *   n_vertices   [B][R]   kept vertices (> max_vertices: truncated)
+ *   workspace    >= pm_region_polygons_workspace_bytes(B, R, max_contour), 256-B aligned */
+PM_API pm_status pm_region_polygons(const int32_t* labels, int32_t W, int32_t H, int32_t n_frames,
+                                    int32_t n_regions, const pm_polygon_params* prm, int32_t* contour_len,
+                                    int32_t* vertices, int32_t* n_vertices, void* workspace, size_t ws_bytes,
+                                    pm_stream_t stream);
+PM_API size_t pm_region_polygons_workspace_bytes(int32_t n_frames, int32_t n_regions, int32_t max_contour);
+
+/* Rasterise the polygons back to labels ("rasterize its interior"):
+ * pixel (x, y) gets the lowest region index whose polygon contains the pixel
+ * centre by the even-odd rule with half-open crossings (Q37, Q38), -1 if
+ * none; polygons with < 3 vertices cover nothing.
+ *   labels_out [B][H][W] int32; workspace >= 16 * B * max(R, 1) bytes, 256-B aligned. */
+PM_API pm_status pm_rasterize_polygons(const int32_t* vertices, const int32_t* n_vertices, int32_t max_vertices,
+                                       int32_t W, int32_t H, int32_t n_frames, int32_t n_regions,
+                                       int32_t* labels_out, void* workspace, size_t ws_bytes, pm_stream_t stream);
+
+/* Lift every polygon vertex onto its region's fitted plane along the camera
+ * ray: X = -d / (n.r) r, r = ((u-cx)/fx, (v-cy)/fy, 1), fp64 (Q39).
+ *   planes [B][R] (from pm_ransac_planes); X_out [B][R][max_vertices][3]
+ *   double, NaN for missing vertices, planes not PM_PLANE_OK, rays parallel
+ *   to the plane or hitting it behind the camera. */
+PM_API pm_status pm_lift_polygon_vertices(const int32_t* vertices, const int32_t* n_vertices,
+                                          int32_t max_vertices, const pm_plane* planes, int32_t n_frames,
+                                          int32_t n_regions, const pm_intrinsics* K, double* X_out,
+                                          pm_stream_t stream);
+
+/* ---------------------------------------------------------------------- */
 /* NEXT-4 of SURVEY §8(f), HOST code (no device work): the paper's map merge
  * gate and vertical-drift Kalman filter (§III-E) applied to the
  * plane table (one plane per region in place of the paper's polygon;

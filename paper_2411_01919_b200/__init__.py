@@ -106,6 +106,8 @@ EXPORTED = ("pm_adf_filter", "pm_adf_filter_batched", "pm_adf_filter_ex", "pm_ad
             "pm_process_frames", "pm_pipeline_workspace_bytes", "pm_pipeline_kernel_launches",
             "pm_process_frames_host", "pm_host_pipeline_arena_bytes", "pm_depth_u16_to_metres",
             "pm_segment_regions", "pm_segment_workspace_bytes",
+            "pm_region_polygons", "pm_region_polygons_workspace_bytes", "pm_rasterize_polygons",
+            "pm_lift_polygon_vertices",
             "pm_drift_kalman_step", "pm_merge_gate", "pm_plane_map_merge_frame",
             "pm_status_string", "pm_version")
 
@@ -432,3 +434,69 @@ class PlaneMap:
     def as_list(self):
         return [{"n": list(p.n), "c": list(p.c), "w": p.w, "n_obs": p.n_obs}
                 for p in self.planes[:self.count.value]]
+
+
+# ---------------------------------------------------------------- NEXT-3
+class pm_polygon_params(ctypes.Structure):
+    _fields_ = [("eps16", _I32), ("max_contour", _I32), ("max_vertices", _I32)]
+
+
+_lib.pm_region_polygons.restype = ctypes.c_int
+_lib.pm_rasterize_polygons.restype = ctypes.c_int
+_lib.pm_lift_polygon_vertices.restype = ctypes.c_int
+_lib.pm_region_polygons_workspace_bytes.restype = _SZ
+_lib.pm_region_polygons_workspace_bytes.argtypes = [_I32, _I32, _I32]
+
+
+class Polygons(NamedTuple):
+    contour_len: torch.Tensor   # int32 [.., R]
+    vertices: torch.Tensor      # int32 [.., R, max_vertices, 2]
+    n_vertices: torch.Tensor    # int32 [.., R]
+
+
+def region_polygons(labels: torch.Tensor, n_regions: int, eps: float = 3.0, max_contour: int = 8192,
+                    max_vertices: int = 256, workspace: torch.Tensor = None) -> Polygons:
+    """NEXT-3: outer contour of every region (Moore
+    tracing) simplified by closed Douglas-Peucker (eps px, exact to 1/16 px)."""
+    B, H, W = _frames(labels, torch.int32)
+    lead = () if labels.dim() == 2 else (B,)
+    dev = labels.device
+    clen = torch.empty(lead + (n_regions,), dtype=torch.int32, device=dev)
+    verts = torch.zeros(lead + (n_regions, max_vertices, 2), dtype=torch.int32, device=dev)
+    nv = torch.empty(lead + (n_regions,), dtype=torch.int32, device=dev)
+    nb = int(_lib.pm_region_polygons_workspace_bytes(B, n_regions, max_contour))
+    ws = workspace if workspace is not None else _workspace(nb, dev)
+    prm = pm_polygon_params(int(round(eps * 16)), int(max_contour), int(max_vertices))
+    _check(_lib.pm_region_polygons(ctypes.c_void_p(labels.data_ptr()), W, H, B, int(n_regions), ctypes.byref(prm),
+                                   ctypes.c_void_p(clen.data_ptr()), ctypes.c_void_p(verts.data_ptr()),
+                                   ctypes.c_void_p(nv.data_ptr()), ctypes.c_void_p(ws.data_ptr()),
+                                   ctypes.c_size_t(ws.numel()), ctypes.c_void_p(_stream(labels))))
+    return Polygons(clen, verts, nv)
+
+
+def rasterize_polygons(polys: Polygons, W: int, H: int, out: torch.Tensor = None) -> torch.Tensor:
+    """Labels [.., H, W] from polygons (lowest region index wins, -1 = none)."""
+    v, nv = polys.vertices, polys.n_vertices
+    single = nv.dim() == 1
+    B = 1 if single else nv.shape[0]
+    R, MV = v.shape[-3], v.shape[-2]
+    out = torch.empty(((H, W) if single else (B, H, W)), dtype=torch.int32, device=v.device) if out is None else out
+    ws = _workspace(16 * B * max(R, 1), v.device)
+    _check(_lib.pm_rasterize_polygons(ctypes.c_void_p(v.data_ptr()), ctypes.c_void_p(nv.data_ptr()), MV, W, H, B, R,
+                                      ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(ws.data_ptr()),
+                                      ctypes.c_size_t(ws.numel()), ctypes.c_void_p(_stream(v))))
+    return out
+
+
+def lift_polygon_vertices(polys: Polygons, planes, K) -> torch.Tensor:
+    """Polygon vertices onto their region planes along camera rays: float64 [.., R, max_vertices, 3]."""
+    v, nv = polys.vertices, polys.n_vertices
+    single = nv.dim() == 1
+    B = 1 if single else nv.shape[0]
+    R, MV = v.shape[-3], v.shape[-2]
+    raw = planes.raw if hasattr(planes, "raw") else planes
+    X = torch.empty(v.shape[:-1] + (3,), dtype=torch.float64, device=v.device)
+    _check(_lib.pm_lift_polygon_vertices(ctypes.c_void_p(v.data_ptr()), ctypes.c_void_p(nv.data_ptr()), MV,
+                                         ctypes.c_void_p(raw.data_ptr()), B, R, ctypes.byref(_K(K)),
+                                         ctypes.c_void_p(X.data_ptr()), ctypes.c_void_p(_stream(v))))
+    return X

@@ -414,3 +414,60 @@ def test_segment_then_ransac_pipeline(pm):
         assert np.array_equal(planes.best_hyp[i].cpu().numpy(), ref["best_hyp"])
         assert np.array_equal(planes.status[i].cpu().numpy(), ref["status"])
         assert (ref["status"][:ref_n] == 0).mean() > 0.5
+
+
+# ------------------------------------------------------------ NEXT-3 polygons
+def _poly_label_images():
+    cv2 = pytest.importorskip("cv2")
+    ims = []
+    fr = scenegen.make_config("C2", noise=False)
+    n = oracle.normals(fr["depth"].numpy(), fr["K"]).astype(np.float32)
+    lab, nr, _ = oracle.segment_regions(n, 30, 90, 300)
+    ims.append((lab, nr, fr))
+    rng = np.random.default_rng(4)
+    H, W = fr["depth"].shape
+    blob = np.full((H, W), -1, np.int32)
+    for r in range(12):                               # random ellipses, later ones painted over earlier
+        m = np.zeros((H, W), np.uint8)
+        cv2.ellipse(m, (int(rng.integers(20, W - 20)), int(rng.integers(20, H - 20))),
+                    (int(rng.integers(3, 60)), int(rng.integers(3, 40))), float(rng.uniform(0, 180)), 0, 360, 1, -1)
+        blob[m > 0] = r
+    ims.append((blob, 12, fr))
+    return ims
+
+
+def test_region_polygons_rasterize_lift_bit_exact(pm):
+    for lab, R, fr in _poly_label_images():
+        H, W = lab.shape
+        labs = np.stack([lab, np.flipud(lab).copy()])          # a batch of two frames
+        polys = pm.region_polygons(torch.from_numpy(labs).to(DEV), R, eps=3.0, max_contour=8192, max_vertices=512)
+        ras = pm.rasterize_polygons(polys, W, H)
+        depth = torch.stack([fr["depth"], fr["depth"].flip(0)]).contiguous().to(DEV)
+        planes = pm.ransac_planes(depth, fr["K"], torch.from_numpy(np.where(labs >= 0, labs, -1)).to(DEV), R, 64,
+                                  0.01, 3)
+        X = pm.lift_polygon_vertices(polys, planes, fr["K"])
+        torch.cuda.synchronize()
+        K32 = scenegen.Intrinsics(*[float(np.float32(v)) for v in (fr["K"].fx, fr["K"].fy, fr["K"].cx, fr["K"].cy)])
+        for b in range(2):
+            ref_polys = []
+            for r in range(R):
+                c = oracle.trace_contour(labs[b], r)
+                assert polys.contour_len[b, r].item() == len(c)
+                s = oracle.simplify_dp(c, 3.0) if len(c) else np.zeros((0, 2), np.int32)
+                m = polys.n_vertices[b, r].item()
+                assert m == len(s)
+                assert np.array_equal(polys.vertices[b, r, :m].cpu().numpy(), s)
+                ref_polys.append(s)
+                raw = planes.raw[b, r].cpu().numpy()
+                if raw[10] == 0 and m:
+                    pl = raw[:4].view(np.float32).astype(np.float64)
+                    Xr = oracle.lift_vertices(s, pl, K32)
+                    Xg = X[b, r, :m].cpu().numpy()
+                    assert np.array_equal(np.isnan(Xg), np.isnan(Xr))
+                    ok = ~np.isnan(Xr)
+                    assert np.abs(Xg[ok] - Xr[ok]).max(initial=0) <= 1e-12
+                else:
+                    assert torch.isnan(X[b, r]).all()
+            want = oracle.rasterize_polygons([p if len(p) >= 3 else np.zeros((0, 2), np.int32) for p in ref_polys],
+                                             W, H)
+            assert np.array_equal(ras[b].cpu().numpy(), want)
