@@ -45,6 +45,9 @@ ADF_ALG_BYTES_PX = 20
 ADF_OPS_PER_PIX_ITER = 11
 # one RANSAC point-hypothesis evaluation: 3 FFMA (n.p + d), compare, count
 RANSAC_OPS_PER_EVAL = 5
+WORKLOAD = ("C4 (BASELINE.json configs[3]): stream of distinct 640x480 D435-noise G-STAIR frames; ADF N=20 "
+            "(lambda 0.15, kappa 0.03 m) + fused normals, RANSAC 64 regions x 64 hypotheses (tau 0.01 m) on the "
+            "filtered depth")
 
 
 def _ncu_traffic():
@@ -192,8 +195,8 @@ def run_reference(args, rank, world):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64+f32",
         "data": "synthetic",
-        "config": {"workload": "C4 (BASELINE.json configs[3]) 640x480 G-STAIR stream, ADF N=20 + normals + "
-                               "RANSAC 64 regions x 64 hyps", "frames_per_step": cores},
+        "config": {"workload": WORKLOAD, "frames_per_step": cores,
+                   "sample": f"{cores} frames of the same stream per step (one per host core)"},
         "cpu_baseline": {"value": value, "unit": "frames/s", "cores": cores, "kind": "oracle",
                          "sample": f"{cores} frames per step (one per core), {args.steps} timed steps"},
         "e2e": {"value": value, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -344,9 +347,7 @@ def run_cuda(args, rank, world, local_rank):
             "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": "C4 (BASELINE.json configs[3]): stream of distinct 640x480 D435-noise G-STAIR "
-                                   "frames; ADF N=20 (lambda 0.15, kappa 0.03 m) + fused normals, RANSAC 64 "
-                                   "regions x 64 hypotheses (tau 0.01 m) on the filtered depth",
+            "config": {"workload": WORKLOAD,
                        "frames_per_rank": B, "global_frames_per_step": world * B,
                        "l2": f"inputs larger than L2 ({B * W * H * 8 / 2**20:.0f} MiB depth+labels per rank)",
                        "parallelism": f"frame-sharded x{world}"},
