@@ -33,9 +33,11 @@ __global__ void __launch_bounds__(kThreads)
 region_start_kernel(const int32_t* __restrict__ labels, int WH, int R, int32_t* __restrict__ start) {
     const size_t f = blockIdx.y;
     const int p = blockIdx.x * kThreads + threadIdx.x;
-    if (p >= WH) return;
-    const int l = labels[f * WH + p];
-    if (l >= 0 && l < R) atomicMin(start + f * R + l, p);
+    const int l = p < WH ? labels[f * WH + p] : -1;
+    // warp-aggregated: the lowest lane of each label group holds the group's
+    // smallest raster index (p grows with the lane); one atomic per group
+    const unsigned m = __match_any_sync(0xFFFFFFFFu, l);
+    if (l >= 0 && l < R && (int)(threadIdx.x & 31) == __ffs(m) - 1) atomicMin(start + f * R + l, p);
 }
 
 __device__ __forceinline__ bool in_region(const int32_t* lab, int W, int H, int x, int y, int r) {
@@ -59,11 +61,16 @@ trace_kernel(const int32_t* __restrict__ labels, int W, int H, int R, const int3
     const int sx = s % W, sy = s / W;
     int px = sx, py = sy, bdir = 4, first_dir = -1, len = 0;
     for (;;) {
-        int found = -1;
-        for (int k = 1; k <= 8; ++k) {
-            const int d = (bdir + k) & 7;
-            if (in_region(lab, W, H, px + kMoore[d][0], py + kMoore[d][1], r)) { found = d; break; }
-        }
+        // all 8 neighbour loads issued together (the step's latency is one
+        // load, not up to eight), then the first region pixel clockwise after
+        // the backtrack direction
+        uint32_t mask = 0;
+#pragma unroll
+        for (int d = 0; d < 8; ++d)
+            mask |= in_region(lab, W, H, px + kMoore[d][0], py + kMoore[d][1], r) ? (1u << d) : 0u;
+        const int s0 = (bdir + 1) & 7;
+        const uint32_t rot = ((mask >> s0) | (mask << (8 - s0))) & 0xFFu;
+        const int found = rot ? (s0 + __ffs(rot) - 1) & 7 : -1;
         if (found < 0) {
             if (cap > 0) out[0] = (uint32_t)px | ((uint32_t)py << 16);
             len = 1;
