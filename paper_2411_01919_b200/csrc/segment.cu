@@ -257,21 +257,36 @@ PM_DEVINL void l_unite(int* lp, int a, int b) {
 __global__ void __launch_bounds__(256)
 seg_local_ccl4(const uint8_t* __restrict__ edge, int W, int H, int* __restrict__ parent) {
     __shared__ int lp[kCT * kCT];
+    __shared__ unsigned rowmask[kCT];
     const size_t f = blockIdx.z;
     const size_t HW = (size_t)W * H;
     const int x0 = blockIdx.x * kCT, y0 = blockIdx.y * kCT;
     const uint8_t* e = edge + f * HW;
-    for (int i = threadIdx.x; i < kCT * kCT; i += 256) {
-        const int ly = i / kCT, lx = i % kCT;
-        const int gy = y0 + ly, gx = x0 + lx;
-        lp[i] = (gy < H && gx < W && e[(size_t)gy * W + gx] == 0) ? i : -1;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    // run start of lane's column in a row mask (first pixel after the last
+    // edge pixel to its left)
+    auto run_start = [&](unsigned m) {
+        const unsigned bg = ~m & ((1u << lane) - 1u);
+        return bg ? 32 - __clz(bg) : 0;
+    };
+    // (1) horizontal runs: one warp per row (kCT = 32 columns), every pixel
+    // points at its run's first pixel, which is the run's root
+    for (int ly = warp; ly < kCT; ly += 8) {
+        const int gy = y0 + ly, gx = x0 + lane;
+        const bool fg = gy < H && gx < W && e[(size_t)gy * W + gx] == 0;
+        const unsigned m = __ballot_sync(0xFFFFFFFFu, fg);
+        if (lane == 0) rowmask[ly] = m;
+        lp[ly * kCT + lane] = fg ? ly * kCT + run_start(m) : -1;
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < kCT * kCT; i += 256) {
-        if (lp[i] < 0) continue;
-        const int ly = i / kCT, lx = i % kCT;
-        if (lx > 0 && lp[i - 1] >= 0) l_unite(lp, i, i - 1);
-        if (ly > 0 && lp[i - kCT] >= 0) l_unite(lp, i, i - kCT);
+    // (2) one union per pair of vertically overlapping runs, at the first
+    // column of their overlap (union by minimum index: canonical roots)
+    for (int ly = 1 + warp; ly < kCT; ly += 8) {
+        const unsigned m = rowmask[ly], mn = rowmask[ly - 1];
+        if (((m & mn) >> lane) & 1u) {
+            const int s = run_start(m), sn = run_start(mn);
+            if (lane == max(s, sn)) l_unite(lp, ly * kCT + s, (ly - 1) * kCT + sn);
+        }
     }
     __syncthreads();
     for (int i = threadIdx.x; i < kCT * kCT; i += 256) {
