@@ -302,6 +302,83 @@ seg_local_ccl4(const uint8_t* __restrict__ edge, int W, int H, int* __restrict__
     }
 }
 
+// Hysteresis components (8-connectivity over Canny candidates, cls & 3 != 0),
+// tile-local first: horizontal runs per row (one warp per row), then one union
+// per pair of 8-adjacent runs in consecutive rows at the first column where
+// they touch (run A in row y touches run B in row y-1 at column x iff B holds
+// one of x-1, x, x+1; the first such x in A is max(sA, sB - 1)).  Roots are
+// the minimum local index (canonical), written as global indices.
+__global__ void __launch_bounds__(256)
+seg_local_ccl8(const uint8_t* __restrict__ cls, int W, int H, int* __restrict__ parent) {
+    __shared__ int lp[kCT * kCT];
+    __shared__ unsigned rowmask[kCT];
+    const size_t f = blockIdx.z;
+    const size_t HW = (size_t)W * H;
+    const int x0 = blockIdx.x * kCT, y0 = blockIdx.y * kCT;
+    const uint8_t* c = cls + f * HW;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    auto start_at = [](unsigned m, int x) {          // run start of column x (x in the run)
+        const unsigned bg = ~m & ((1u << x) - 1u);
+        return bg ? 32 - __clz(bg) : 0;
+    };
+    for (int ly = warp; ly < kCT; ly += 8) {
+        const int gy = y0 + ly, gx = x0 + lane;
+        const bool fg = gy < H && gx < W && (c[(size_t)gy * W + gx] & 3) != 0;
+        const unsigned m = __ballot_sync(0xFFFFFFFFu, fg);
+        if (lane == 0) rowmask[ly] = m;
+        lp[ly * kCT + lane] = fg ? ly * kCT + start_at(m, lane) : -1;
+    }
+    __syncthreads();
+    for (int ly = 1 + warp; ly < kCT; ly += 8) {
+        const unsigned m = rowmask[ly], mn = rowmask[ly - 1];
+        if (!((m >> lane) & 1u)) continue;
+        const int sA = start_at(m, lane);
+#pragma unroll
+        for (int dx = -1; dx <= 1; ++dx) {
+            const int p = lane + dx;
+            if (p < 0 || p >= 32 || !((mn >> p) & 1u)) continue;
+            const int sB = start_at(mn, p);
+            if (lane == max(sA, sB - 1)) l_unite(lp, ly * kCT + sA, (ly - 1) * kCT + sB);
+        }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < kCT * kCT; i += 256) {
+        const int ly = i / kCT, lx = i % kCT;
+        const int gy = y0 + ly, gx = x0 + lx;
+        if (gy >= H || gx >= W) continue;
+        int g = -1;
+        if (lp[i] >= 0) {
+            const int r = l_find(lp, i);
+            g = (y0 + r / kCT) * W + (x0 + r % kCT);
+        }
+        parent[f * HW + (size_t)gy * W + gx] = g;
+    }
+}
+
+// 8-connected merge across tile borders: pixels of a tile's west column and
+// north row unite with their W, NW, N, NE neighbours in other tiles
+__global__ void __launch_bounds__(kT)
+seg_border_merge8(int W, int H, int* __restrict__ parent) {
+    const size_t i = (size_t)blockIdx.x * kT + threadIdx.x;
+    const size_t f = blockIdx.y;
+    const size_t HW = (size_t)W * H;
+    if (i >= HW) return;
+    const int v = (int)(i / W), u = (int)(i % W);
+    const bool west = u > 0 && (u % kCT) == 0, north = v > 0 && (v % kCT) == 0;
+    const bool east_edge = u < W - 1 && ((u + 1) % kCT) == 0;   // NE neighbour in the next tile column
+    if (!west && !north && !(east_edge && v > 0)) return;
+    int* par = parent + f * HW;
+    if (__ldcg(par + i) < 0) return;
+    if (west && __ldcg(par + i - 1) >= 0) uf_unite(par, (int)i, (int)i - 1);
+    if (v > 0) {
+        // NW crosses a border if west or north; N if north; NE if north or east_edge
+        if (u > 0 && (west || north) && __ldcg(par + i - W - 1) >= 0) uf_unite(par, (int)i, (int)(i - W - 1));
+        if (north && __ldcg(par + i - W) >= 0) uf_unite(par, (int)i, (int)(i - W));
+        if (u < W - 1 && (north || east_edge) && __ldcg(par + i - W + 1) >= 0)
+            uf_unite(par, (int)i, (int)(i - W + 1));
+    }
+}
+
 // global merge across tile borders (west column and north row of each tile)
 __global__ void __launch_bounds__(kT)
 seg_border_merge4(int W, int H, int* __restrict__ parent) {
@@ -429,8 +506,8 @@ PM_API pm_status pm_segment_regions(const float* normals, int32_t W, int32_t H, 
     seg_candidates_kernel<<<dim3((W + kTW - 1) / kTW, (H + kTH - 1) / kTH, n_frames), dim3(kTX, kTY), 0, s>>>(
         normals, W, H, low2, high2, L.cls);
     // hysteresis: components of candidates (8-conn) containing a strong pixel
-    seg_uf_init<0><<<gp, kT, 0, s>>>(L.cls, HW, L.parent);
-    seg_uf_merge<0><<<gp, kT, 0, s>>>(W, H, L.parent);
+    seg_local_ccl8<<<dim3((W + kCT - 1) / kCT, (H + kCT - 1) / kCT, n_frames), 256, 0, s>>>(L.cls, W, H, L.parent);
+    seg_border_merge8<<<gp, kT, 0, s>>>(W, H, L.parent);
     seg_uf_flatten<<<gp, kT, 0, s>>>(HW, L.parent);
     if (cudaMemsetAsync(L.aux, 0, sizeof(int) * bytes, s) != cudaSuccess) return PM_ERR_CUDA;
     seg_strong<<<gp, kT, 0, s>>>(L.cls, HW, L.parent, L.aux);
