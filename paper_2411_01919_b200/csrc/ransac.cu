@@ -1,17 +1,23 @@
 // ransac.cu — Algorithm 2 of arXiv 2411.01919, batched over every
-// region of every frame in three launches:
-//   hyp    : one thread per (frame, region, hypothesis): Philox sample ->
-//            3 points -> f32 plane (Alg. 2 ℓ6-7)
-//   score  : the hot loop (ℓ9-13).  The compacted points of a frame are cut
-//            into fixed chunks, one CTA per chunk regardless of region sizes
-//            (load balance); a chunk's points are deprojected once into
-//            shared memory and scored against every hypothesis of the
-//            region(s) it overlaps, 8 hypotheses per register block; counts
-//            are warp-reduced (REDUX) and added to global integer counters
-//            (exact, order-free)
-//   select : one CTA per (frame, region): argmax count (ties -> lowest h,
-//            ℓ14-17), fp64 least-squares refit over the winner's inliers, gate
-//            (ℓ19), pm_plane output.
+// region of every frame in five launches:
+//   hyp      : one thread per (frame, region, hypothesis): Philox sample ->
+//              3 points -> f32 plane (Alg. 2 ℓ6-7); also the plane pairs
+//              (h, h + L) the packed scoring loop reads
+//   score    : the hot loop (ℓ9-13).  The compacted points of a frame are cut
+//              into fixed 4096-point chunks, one CTA per chunk regardless of
+//              region sizes (load balance); a chunk's points are deprojected
+//              once into shared memory and scored against every hypothesis
+//              of the region(s) it overlaps: K hypotheses per lane in
+//              registers, two per packed FFMA2 chain; counts reduced by
+//              shuffles + shared memory and added to global integer counters
+//              with one atomic per hypothesis (exact, order-free)
+//   select   : one warp per (frame, region): argmax count (or argmin error),
+//              ties -> lowest h (ℓ14-17)
+//   refit    : 8192-point chunks: the winner's inliers recounted with the same
+//              f32 arithmetic, fp64 shifted moments, one slot per (chunk +
+//              region, warp) -- no float atomics
+//   finalize : one thread per (frame, region): slots summed in a fixed order,
+//              3x3 eigen-solve, gate (ℓ19), pm_plane output.
 // All plane and distance arithmetic uses explicit _rn intrinsics in the f32
 // order DESIGN.md §3 fixes, so counts are bit-identical to the oracle's.
 #include <cuda_runtime.h>
