@@ -25,7 +25,7 @@ namespace pm {
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int32_t kNoStart = 0x7FFFFFFF;
+constexpr int32_t kNoStart = 0x7F7F7F7F;   // the byte-wise memset fill of `start` (no pixel)
 
 __device__ __constant__ int kMoore[8][2] = {{1, 0}, {1, 1}, {0, 1}, {-1, 1}, {-1, 0}, {-1, -1}, {0, -1}, {1, -1}};
 

@@ -88,3 +88,33 @@ def test_product_never_imports_oracle():
                 txt = open(os.path.join(dirpath, f), errors="ignore").read()
                 assert "import oracle" not in txt and "from oracle" not in txt and "oracle.h" not in txt, f
                 assert "liboracle" not in txt, f
+
+
+def test_next_features_reject_bad_arguments_before_launch(pm):
+    """NEXT-3 polygon calls and the host pipeline's label formats validate on
+    the host (no device work)."""
+    L = pm._lib
+    v = ctypes.c_void_p
+    bogus, other, ws = v(0x1000), v(0x100000000), v(0x300000000)
+    prm = pm.pm_polygon_params(48, 8192, 256)
+    assert L.pm_region_polygons(None, 640, 480, 1, 64, ctypes.byref(prm), bogus, bogus, bogus, ws, ctypes.c_size_t(1 << 40),
+                                None) == 1
+    bad = pm.pm_polygon_params(48, 8192, 2)                 # < 3 vertices
+    assert L.pm_region_polygons(bogus, 640, 480, 1, 64, ctypes.byref(bad), bogus, bogus, bogus, ws,
+                                ctypes.c_size_t(1 << 40), None) == 1
+    assert L.pm_region_polygons(bogus, 640, 480, 1, 64, ctypes.byref(prm), bogus, bogus, bogus, ws, ctypes.c_size_t(16),
+                                None) == 2
+    assert L.pm_region_polygons(bogus, 640, 480, 1, 0, ctypes.byref(prm), bogus, bogus, bogus, None, ctypes.c_size_t(0),
+                                None) == 0                   # no regions: no-op
+    assert L.pm_region_polygons_workspace_bytes(4, 64, 8192) >= 4 * 64 * 8192 * 4
+    assert L.pm_rasterize_polygons(bogus, bogus, 2, 640, 480, 1, 64, bogus, ws, ctypes.c_size_t(1 << 20), None) == 1
+    assert L.pm_rasterize_polygons(bogus, bogus, 16, 640, 480, 1, 64, bogus, ws, ctypes.c_size_t(8), None) == 2
+    K = pm.pm_intrinsics(385.0, 385.0, 319.5, 239.5)
+    assert L.pm_lift_polygon_vertices(bogus, bogus, 16, None, 1, 64, ctypes.byref(K), bogus, None) == 1
+    # host pipeline: uint8 labels allow at most 255 regions; unknown formats rejected
+    big = ctypes.c_size_t(1 << 40)
+    args = lambda lf, R: (other, 1, other, lf, 640, 480, 8, 0, ctypes.byref(K), ctypes.c_float(0.15),
+                          ctypes.c_float(0.03), 20, R, 64, ctypes.c_float(0.01), ctypes.c_uint64(1), other, None,
+                          None, 8, ws, big, None)
+    assert L.pm_process_frames_host(*args(pm.LABELS_U8, 256)) == 1
+    assert L.pm_process_frames_host(*args(7, 64)) == 1

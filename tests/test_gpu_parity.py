@@ -471,3 +471,27 @@ def test_region_polygons_rasterize_lift_bit_exact(pm):
             want = oracle.rasterize_polygons([p if len(p) >= 3 else np.zeros((0, 2), np.int32) for p in ref_polys],
                                              W, H)
             assert np.array_equal(ras[b].cpu().numpy(), want)
+
+
+def test_region_polygons_edge_cases(pm):
+    # empty regions, a single pixel, a two-pixel region, a region touching the
+    # image border, contour capacity below the traced length
+    lab = np.full((40, 50), -1, np.int32)
+    lab[5, 5] = 1
+    lab[9, 9:11] = 2
+    lab[20:40, 0:50] = 4                      # touches three image borders
+    polys = pm.region_polygons(torch.from_numpy(lab).to(DEV), 6, eps=1.0, max_contour=4096, max_vertices=64)
+    small = pm.region_polygons(torch.from_numpy(lab).to(DEV), 6, eps=1.0, max_contour=16, max_vertices=64)
+    ras = pm.rasterize_polygons(polys, 50, 40)
+    torch.cuda.synchronize()
+    for r in range(6):
+        c = oracle.trace_contour(lab, r)
+        assert polys.contour_len[r].item() == len(c) == small.contour_len[r].item()
+        s = oracle.simplify_dp(c, 1.0) if len(c) else np.zeros((0, 2), np.int32)
+        m = polys.n_vertices[r].item()
+        assert m == len(s) and np.array_equal(polys.vertices[r, :m].cpu().numpy(), s)
+    assert polys.n_vertices[0].item() == 0 and polys.n_vertices[3].item() == 0
+    want = oracle.rasterize_polygons([polys.vertices[r, :polys.n_vertices[r].item()].cpu().numpy()
+                                      if polys.n_vertices[r].item() >= 3 else np.zeros((0, 2), np.int32)
+                                      for r in range(6)], 50, 40)
+    assert np.array_equal(ras.cpu().numpy(), want)
