@@ -219,65 +219,56 @@ PM_DEVINL void sweep_pairs(const float* __restrict__ cur, float* __restrict__ nx
     auto ld2 = [](const float* a) { return *reinterpret_cast<const float2*>(a); };
     float2 C = ld2(col);
     float2 N = ys == b.iy0 ? C : ld2(col - kSW);
-    if (!CHECK) {
-        // packed path, software-pipelined: the next row's S, W, E are loaded
-        // before this row's store (loads are not hoisted above a possibly
-        // aliasing store).  The last step prefetches one row past the region
-        // (at most row SH: the buffers carry one spare row), never used.
-        const int n = ymid - ys;
-        float2 S = ld2(col + kSW);
-        float2 P = make_float2(colW[0], colE[0]);
-        auto step = [&]() {
-            const float2 S1 = ld2(col + 2 * kSW);
-            const float2 P1 = make_float2(colW[kSW], colE[kSW]);
-            *reinterpret_cast<float2*>(ocol) = cell2<DIV>(C, N, S, P, make_float2(C.y, C.x), p);
-            N = C;
-            C = S;
-            S = S1;
-            P = P1;
-            col += kSW;
-            colW += kSW;
-            colE += kSW;
-            ocol += kSW;
-        };
-        int i = 0;
-        for (; i + 4 <= n; i += 4) {
-            step(); step(); step(); step();
-        }
-        if (i < n) {                                // 0-3 last rows, straight-line
-            step();
-            if (i + 1 < n) {
-                step();
-                if (i + 2 < n) step();
-            }
-        }
-        if (ye > ylast)                           // last image row: S = C
-            *reinterpret_cast<float2*>(ocol) = cell2<DIV>(C, N, C, P, make_float2(C.y, C.x), p);
-        return;
-    }
-    int y = ys;
-#pragma unroll 4
-    for (; y < ymid; ++y) {
-        const float2 S = ld2(col + kSW);
-        const float W = colW[0];
-        const float E = colE[0];
-        float2 o;
-        o.x = cell<CHECK, DIV>(C.x, N.x, S.x, W, C.y, p);
-        o.y = cell<CHECK, DIV>(C.y, N.y, S.y, C.x, E, p);
-        *reinterpret_cast<float2*>(ocol) = o;
+    // The cell pair in packed FP32.  CHECK (tiles with invalid depth, Q4):
+    // every invalid neighbour -- outer (P) or inner (the other cell of the
+    // pair, in Cs) -- is replaced by the centre (zero flux) and invalid
+    // centres keep their value: the substitution of cell<true>, so both
+    // cells still get the scalar rounding sequence.
+    auto cellp = [&](float2 C, float2 N, float2 S, float2 P) -> float2 {
+        if (!CHECK) return cell2<DIV>(C, N, S, P, make_float2(C.y, C.x), p);
+        const bool vx = valid_depth(C.x), vy = valid_depth(C.y);
+        const float2 Nv = make_float2(valid_depth(N.x) ? N.x : C.x, valid_depth(N.y) ? N.y : C.y);
+        const float2 Sv = make_float2(valid_depth(S.x) ? S.x : C.x, valid_depth(S.y) ? S.y : C.y);
+        const float2 Pv = make_float2(valid_depth(P.x) ? P.x : C.x, valid_depth(P.y) ? P.y : C.y);
+        const float2 Cs = make_float2(vy ? C.y : C.x, vx ? C.x : C.y);
+        float2 o = cell2<DIV>(C, Nv, Sv, Pv, Cs, p);
+        o.x = vx ? o.x : C.x;
+        o.y = vy ? o.y : C.y;
+        return o;
+    };
+    // software-pipelined: the next row's S, W, E are loaded before this row's
+    // store (loads are not hoisted above a possibly aliasing store).  The last
+    // step prefetches one row past the region (at most row SH: the buffers
+    // carry one spare row), never used.
+    const int n = ymid - ys;
+    float2 S = ld2(col + kSW);
+    float2 P = make_float2(colW[0], colE[0]);
+    auto step = [&]() {
+        const float2 S1 = ld2(col + 2 * kSW);
+        const float2 P1 = make_float2(colW[kSW], colE[kSW]);
+        *reinterpret_cast<float2*>(ocol) = cellp(C, N, S, P);
         N = C;
         C = S;
+        S = S1;
+        P = P1;
         col += kSW;
         colW += kSW;
         colE += kSW;
         ocol += kSW;
+    };
+    int i = 0;
+    for (; i + 4 <= n; i += 4) {
+        step(); step(); step(); step();
     }
-    if (ye > ylast) {                               // last image row: S = C
-        float2 o;
-        o.x = cell<CHECK, DIV>(C.x, N.x, C.x, colW[0], C.y, p);
-        o.y = cell<CHECK, DIV>(C.y, N.y, C.y, C.x, colE[0], p);
-        *reinterpret_cast<float2*>(ocol) = o;
+    if (i < n) {                                    // 0-3 last rows, straight-line
+        step();
+        if (i + 1 < n) {
+            step();
+            if (i + 2 < n) step();
+        }
     }
+    if (ye > ylast)                                 // last image row: S = C
+        *reinterpret_cast<float2*>(ocol) = cellp(C, N, C, P);
 }
 
 // Sobel (1/8-normalised, clamp-to-edge) + geometric normal (Eq. 2 read as
