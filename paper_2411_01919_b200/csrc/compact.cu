@@ -26,7 +26,7 @@ namespace {
 
 constexpr unsigned kFull = 0xFFFFFFFFu;
 constexpr int kWarpsPerBlock = 8;
-constexpr int kPrefetch = 4;          // 32-pixel steps whose loads are issued together
+constexpr int kPrefetch = 8;          // 32-pixel steps whose loads are issued together
 
 PM_DEVINL unsigned lanemask_lt() {
     unsigned m;
