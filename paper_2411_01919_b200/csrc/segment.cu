@@ -140,34 +140,6 @@ PM_DEVINL void uf_unite(int* parent, int a, int b) {
 
 constexpr int kT = 256;
 
-// mode 0: hysteresis set (cls & 3) != 0, 8-connectivity; mode 1: non-edge pixels, 4-connectivity
-template <int MODE>
-__global__ void __launch_bounds__(kT) seg_uf_init(const uint8_t* __restrict__ m, int HW, int* __restrict__ parent) {
-    const size_t i = (size_t)blockIdx.x * kT + threadIdx.x;
-    const size_t f = blockIdx.y;
-    if (i >= (size_t)HW) return;
-    const uint8_t v = m[f * HW + i];
-    const bool in = MODE == 0 ? (v & 3) != 0 : v == 0;
-    parent[f * HW + i] = in ? (int)i : -1;
-}
-
-template <int MODE>
-__global__ void __launch_bounds__(kT) seg_uf_merge(int W, int H, int* __restrict__ parent) {
-    const size_t i = (size_t)blockIdx.x * kT + threadIdx.x;
-    const size_t f = blockIdx.y;
-    const size_t HW = (size_t)W * H;
-    if (i >= HW) return;
-    int* par = parent + f * HW;
-    if (__ldcg(par + i) < 0) return;
-    const int v = (int)(i / W), u = (int)(i % W);
-    // previous neighbours only (each pair once): W, N (+ NW, NE for 8-connectivity)
-    if (u > 0 && __ldcg(par + i - 1) >= 0) uf_unite(par, (int)i, (int)i - 1);
-    if (v > 0 && __ldcg(par + i - W) >= 0) uf_unite(par, (int)i, (int)(i - W));
-    if (MODE == 0 && v > 0) {
-        if (u > 0 && __ldcg(par + i - W - 1) >= 0) uf_unite(par, (int)i, (int)(i - W - 1));
-        if (u < W - 1 && __ldcg(par + i - W + 1) >= 0) uf_unite(par, (int)i, (int)(i - W + 1));
-    }
-}
 
 __global__ void __launch_bounds__(kT) seg_uf_flatten(int HW, int* __restrict__ parent) {
     const size_t i = (size_t)blockIdx.x * kT + threadIdx.x;
