@@ -151,6 +151,17 @@ def _oracle_frame(depth_np, labels_np, K, frame_id):
     oracle.ransac(d, labels_np, K, REGIONS, HYPS, TAU, SEED, frame_id=frame_id)
 
 
+def _cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 def _cpu_cores():
     try:
         return len(os.sched_getaffinity(0))
@@ -198,7 +209,8 @@ def run_reference(args, rank, world):
         "config": {"workload": WORKLOAD, "frames_per_step": cores,
                    "sample": f"{cores} frames of the same stream per step (one per host core)"},
         "cpu_baseline": {"value": value, "unit": "frames/s", "cores": cores, "kind": "oracle",
-                         "sample": f"{cores} frames per step (one per core), {args.steps} timed steps"},
+                         "sample": f"{cores} frames per step (one per core), {args.steps} timed steps",
+                         "cpu_model": _cpu_model()},
         "e2e": {"value": value, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -339,7 +351,7 @@ def run_cuda(args, rank, world, local_rank):
         fps, wall = _oracle_throughput(frames, K, first, cores)
         cpu = {"value": fps, "unit": "frames/s", "cores": cores, "kind": "oracle",
                "sample": f"{n} frames of the same stream ({wall:.1f} s wall, ~{t1 * n:.0f} s of CPU work; "
-                         f"1 frame on 1 core: {t1 * 1e3:.0f} ms)"}
+                         f"1 frame on 1 core: {t1 * 1e3:.0f} ms)", "cpu_model": _cpu_model()}
 
     launches_per_step = pm.pipeline_kernel_launches(ITERS, REGIONS)
     if rank == 0:
