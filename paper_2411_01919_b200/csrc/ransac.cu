@@ -13,9 +13,10 @@
 //              with one atomic per hypothesis (exact, order-free)
 //   select   : one warp per (frame, region): argmax count (or argmin error),
 //              ties -> lowest h (ℓ14-17)
-//   refit    : 8192-point chunks: the winner's inliers recounted with the same
-//              f32 arithmetic, fp64 shifted moments, one slot per (chunk +
-//              region, warp) -- no float atomics
+//   refit    : 8192-point chunks, 1024 contiguous points per warp: the
+//              winner's inliers recounted with the same f32 arithmetic, fp64
+//              shifted moments, one slot per (chunk + region, warp) -- no
+//              float atomics
 //   finalize : one thread per (frame, region): slots summed in a fixed order,
 //              3x3 eigen-solve, gate (ℓ19), pm_plane output.
 // All plane and distance arithmetic uses explicit _rn intrinsics in the f32
@@ -426,43 +427,52 @@ ransac_refit_kernel(RansacWorkspace ws, RansacArgs a) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const uint2* pts = ws.points + f * (size_t)ws.W * ws.H;
     const float ifx = 1.0f / a.K.fx, ify = 1.0f / a.K.fy;
+    // warp w owns the contiguous sub-chunk [wlo, whi): it meets one or two
+    // regions, so a warp runs ~1.2 moment reductions per chunk instead of one
+    // per region of the chunk
+    constexpr int kWarpSpan = kRefitChunk / kRefitWarps;
+    const int wlo = cs + w * kWarpSpan, whi = min(wlo + kWarpSpan, ce);
     for (int r = s_r0; r < R && off[r] < ce; ++r) {
         const int lo = max(cs, off[r]), hi = min(ce, off[r + 1]);
         if (hi <= lo) continue;
         const int best = ws.best[f * R + r];
         if (best >= 0) {
-            const float4 pl = ws.planes[(f * R + r) * HP + best];
-            const uint2 q0 = pts[off[r]];
-            const float3 o3 = deproject(PackedPoint{q0.x, __uint_as_float(q0.y)}, a.K.cx, a.K.cy, ifx, ify);
-            const double ox = o3.x, oy = o3.y, oz = o3.z;
+            const int a0 = max(lo, wlo), a1 = min(hi, whi);
             Sums acc = {};
-            constexpr int kU = 8;                             // loads in flight per thread
-            for (int i0 = lo + threadIdx.x; i0 < hi; i0 += kU * kScoreThreads) {
-                uint2 qs[kU];
+            if (a0 < a1) {                                    // warp-uniform
+                const float4 pl = ws.planes[(f * R + r) * HP + best];
+                const uint2 q0 = pts[off[r]];
+                const float3 o3 = deproject(PackedPoint{q0.x, __uint_as_float(q0.y)}, a.K.cx, a.K.cy, ifx, ify);
+                const double ox = o3.x, oy = o3.y, oz = o3.z;
+                constexpr int kU = 8;                             // loads in flight per thread
+                for (int i0 = a0 + lane; i0 < a1; i0 += kU * 32) {
+                    uint2 qs[kU];
 #pragma unroll
-                for (int u = 0; u < kU; ++u) {
-                    const int i = i0 + u * kScoreThreads;
-                    qs[u] = i < hi ? __ldg(pts + i) : make_uint2(0u, 0u);
-                }
+                    for (int u = 0; u < kU; ++u) {
+                        const int i = i0 + u * 32;
+                        qs[u] = i < a1 ? __ldg(pts + i) : make_uint2(0u, 0u);
+                    }
 #pragma unroll
-                for (int u = 0; u < kU; ++u) {
-                    if (i0 + u * kScoreThreads >= hi) break;
-                    const float3 P = deproject(PackedPoint{qs[u].x, __uint_as_float(qs[u].y)}, a.K.cx, a.K.cy, ifx, ify);
-                    const float dist = plane_dist(pl, P);
-                    acc.err += __float2ull_rn(__fmul_rn(fminf(dist, 64.0f), 16777216.0f));
-                    if (dist < a.tau) {
-                        const double x = (double)P.x - ox, y = (double)P.y - oy, z = (double)P.z - oz;
-                        acc.s[0] += x; acc.s[1] += y; acc.s[2] += z;
-                        acc.m[0] = fma(x, x, acc.m[0]); acc.m[1] = fma(x, y, acc.m[1]); acc.m[2] = fma(x, z, acc.m[2]);
-                        acc.m[3] = fma(y, y, acc.m[3]); acc.m[4] = fma(y, z, acc.m[4]); acc.m[5] = fma(z, z, acc.m[5]);
-                        acc.n += 1;
+                    for (int u = 0; u < kU; ++u) {
+                        if (i0 + u * 32 >= a1) break;
+                        const float3 P = deproject(PackedPoint{qs[u].x, __uint_as_float(qs[u].y)}, a.K.cx, a.K.cy, ifx, ify);
+                        const float dist = plane_dist(pl, P);
+                        acc.err += __float2ull_rn(__fmul_rn(fminf(dist, 64.0f), 16777216.0f));
+                        if (dist < a.tau) {
+                            const double x = (double)P.x - ox, y = (double)P.y - oy, z = (double)P.z - oz;
+                            acc.s[0] += x; acc.s[1] += y; acc.s[2] += z;
+                            acc.m[0] = fma(x, x, acc.m[0]); acc.m[1] = fma(x, y, acc.m[1]); acc.m[2] = fma(x, z, acc.m[2]);
+                            acc.m[3] = fma(y, y, acc.m[3]); acc.m[4] = fma(y, z, acc.m[4]); acc.m[5] = fma(z, z, acc.m[5]);
+                            acc.n += 1;
+                        }
                     }
                 }
-            }
-            // one slot per (chunk + region, warp): no block barrier; the
-            // finalize kernel sums them in (chunk, warp) order (deterministic)
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) sums_add(acc, sums_shfl_xor(acc, o));
+                for (int o = 16; o > 0; o >>= 1) sums_add(acc, sums_shfl_xor(acc, o));
+            }
+            // one slot per (chunk + region, warp), zero when the warp's span
+            // misses the region: no block barrier; the finalize kernel sums
+            // them in (chunk, warp) order (deterministic)
             if (lane == 0) ws.slots[(f * (size_t)ws.n_slots + blockIdx.x + r) * kRefitWarps + w] = acc;
         }
     }
