@@ -405,8 +405,29 @@ ransac_select_kernel(RansacWorkspace ws, RansacArgs a) {
 // grid = (ceil(W*H / kRefitChunk), B).  For every region segment of the
 // chunk: take the winner (ransac_select_kernel), recount its inliers with the same f32
 // arithmetic, accumulate fp64 moments, write slot (chunk + region).
+// Warp w owns the contiguous sub-chunk [wlo, whi) of kWarpSpan points; it meets
+// one or two regions, so a warp runs ~1.2 moment reductions per chunk.  Its
+// points arrive in shared memory by two bulk copies (cp.async.bulk, one per
+// half span, each on its own mbarrier) issued before any arithmetic, so the
+// second half streams in while the first is processed and the whole chunk is
+// in flight at once (64 KB per CTA) instead of 8 loads per thread.
+constexpr int kWarpSpan = kRefitChunk / kRefitWarps;       // 1024 points
+constexpr int kHalfSpan = kWarpSpan / 2;
+constexpr int kHalfSlot = kHalfSpan + 2;                    // + 16 B alignment slack
+constexpr size_t kRefitSmem = sizeof(uint2) * kRefitWarps * 2 * kHalfSlot;
+
+PM_DEVINL void bulk_load_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"((uint64_t)src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
 __global__ void __launch_bounds__(kScoreThreads)
 ransac_refit_kernel(RansacWorkspace ws, RansacArgs a) {
+    extern __shared__ __align__(16) uint2 s_pts[];            // [warp][half][kHalfSlot]
+    __shared__ __align__(8) uint64_t s_bar[kRefitWarps][2];
     __shared__ int s_r0;
     const size_t f = blockIdx.y;
     const int R = ws.R, HP = ws.n_hyp_pad;
@@ -415,23 +436,40 @@ ransac_refit_kernel(RansacWorkspace ws, RansacArgs a) {
     const int cs = blockIdx.x * kRefitChunk;
     if (cs >= total) return;
     const int ce = min(cs + kRefitChunk, total);
-    if (threadIdx.x == 0) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const uint2* pts = ws.points + f * (size_t)ws.W * ws.H;
+    const int wlo = cs + w * kWarpSpan, whi = min(wlo + kWarpSpan, ce), wmid = min(wlo + kHalfSpan, whi);
+    // half h covers [hs[h], he[h]); its first point sits at s_pts index sb[h] + sh[h]
+    const int hs0 = wlo, he0 = wmid, hs1 = wmid, he1 = whi;
+    uint2* sb0 = s_pts + (w * 2 + 0) * kHalfSlot;
+    uint2* sb1 = s_pts + (w * 2 + 1) * kHalfSlot;
+    // the workspace is 256-B aligned, so a point's byte address is 8-B aligned:
+    // copy from the 16-B boundary at or below it (the extra point is unused;
+    // the rounded-up end stays inside the points buffer's 256-B padding)
+    const int sh0 = (int)(((uintptr_t)(pts + hs0) >> 3) & 1), sh1 = (int)(((uintptr_t)(pts + hs1) >> 3) & 1);
+    if (lane == 0) {
+        mbar_init(&s_bar[w][0], 1);
+        mbar_init(&s_bar[w][1], 1);
+        if (he0 > hs0) {
+            const uint32_t bytes = (uint32_t)(((he0 - hs0 + sh0) * 8 + 15) & ~15);
+            mbar_arrive_expect_tx(&s_bar[w][0], bytes);
+            bulk_load_g2s(sb0, pts + hs0 - sh0, bytes, &s_bar[w][0]);
+        }
+        if (he1 > hs1) {
+            const uint32_t bytes = (uint32_t)(((he1 - hs1 + sh1) * 8 + 15) & ~15);
+            mbar_arrive_expect_tx(&s_bar[w][1], bytes);
+            bulk_load_g2s(sb1, pts + hs1 - sh1, bytes, &s_bar[w][1]);
+        }
         int lo = 0, hi = R;
         while (hi - lo > 1) {
             const int mid = (lo + hi) >> 1;
             if (off[mid] <= cs) lo = mid; else hi = mid;
         }
-        s_r0 = lo;
+        if (w == 0) s_r0 = lo;
     }
-    __syncthreads();
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const uint2* pts = ws.points + f * (size_t)ws.W * ws.H;
+    __syncthreads();          // region start and the mbarrier inits visible to every warp
     const float ifx = 1.0f / a.K.fx, ify = 1.0f / a.K.fy;
-    // warp w owns the contiguous sub-chunk [wlo, whi): it meets one or two
-    // regions, so a warp runs ~1.2 moment reductions per chunk instead of one
-    // per region of the chunk
-    constexpr int kWarpSpan = kRefitChunk / kRefitWarps;
-    const int wlo = cs + w * kWarpSpan, whi = min(wlo + kWarpSpan, ce);
+    int ready = 0;                                           // bit h: half h waited on
     for (int r = s_r0; r < R && off[r] < ce; ++r) {
         const int lo = max(cs, off[r]), hi = min(ce, off[r + 1]);
         if (hi <= lo) continue;
@@ -444,18 +482,16 @@ ransac_refit_kernel(RansacWorkspace ws, RansacArgs a) {
                 const uint2 q0 = pts[off[r]];
                 const float3 o3 = deproject(PackedPoint{q0.x, __uint_as_float(q0.y)}, a.K.cx, a.K.cy, ifx, ify);
                 const double ox = o3.x, oy = o3.y, oz = o3.z;
-                constexpr int kU = 8;                             // loads in flight per thread
-                for (int i0 = a0 + lane; i0 < a1; i0 += kU * 32) {
-                    uint2 qs[kU];
-#pragma unroll
-                    for (int u = 0; u < kU; ++u) {
-                        const int i = i0 + u * 32;
-                        qs[u] = i < a1 ? __ldg(pts + i) : make_uint2(0u, 0u);
-                    }
-#pragma unroll
-                    for (int u = 0; u < kU; ++u) {
-                        if (i0 + u * 32 >= a1) break;
-                        const float3 P = deproject(PackedPoint{qs[u].x, __uint_as_float(qs[u].y)}, a.K.cx, a.K.cy, ifx, ify);
+#pragma unroll 1
+                for (int half = 0; half < 2; ++half) {
+                    const int b0 = max(a0, half ? hs1 : hs0), b1 = min(a1, half ? he1 : he0);
+                    if (b0 >= b1) continue;
+                    if (!(ready >> half & 1)) { mbar_wait(&s_bar[w][half], 0); ready |= 1 << half; }
+                    const uint2* sp = (half ? sb1 + sh1 - hs1 : sb0 + sh0 - hs0);
+#pragma unroll 4
+                    for (int i = b0 + lane; i < b1; i += 32) {
+                        const uint2 q = sp[i];
+                        const float3 P = deproject(PackedPoint{q.x, __uint_as_float(q.y)}, a.K.cx, a.K.cy, ifx, ify);
                         const float dist = plane_dist(pl, P);
                         acc.err += __float2ull_rn(__fmul_rn(fminf(dist, 64.0f), 16777216.0f));
                         if (dist < a.tau) {
@@ -476,6 +512,9 @@ ransac_refit_kernel(RansacWorkspace ws, RansacArgs a) {
             if (lane == 0) ws.slots[(f * (size_t)ws.n_slots + blockIdx.x + r) * kRefitWarps + w] = acc;
         }
     }
+    // a warp whose copies were never waited on must not exit with them in flight
+    if (!(ready & 1) && he0 > hs0) mbar_wait(&s_bar[w][0], 0);
+    if (!(ready & 2) && he1 > hs1) mbar_wait(&s_bar[w][1], 0);
 }
 
 // Smallest-eigenvalue eigenvector of a symmetric 3x3 (double) by cyclic
@@ -608,6 +647,9 @@ cudaError_t ransac_setup_attributes() {
     PM_ATTR(1, 8) PM_ATTR(2, 8) PM_ATTR(4, 8) PM_ATTR(8, 8) PM_ATTR(8, 16) PM_ATTR(8, 32)
     PM_ATTR(8, 64) PM_ATTR(8, 128) PM_ATTR(8, 256) PM_ATTR(16, 256)
 #undef PM_ATTR
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute((const void*)ransac_refit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)kRefitSmem);
     return e;
 }
 
@@ -670,7 +712,7 @@ cudaError_t ransac_run(const RansacWorkspace& ws, const RansacArgs& a, pm_plane*
     if (!launched) return cudaErrorInvalidConfiguration;
     const dim3 g_refit((unsigned)(((size_t)ws.W * ws.H + kRefitChunk - 1) / kRefitChunk), ws.B);
     ransac_select_kernel<<<dim3((ws.R + 7) / 8, ws.B), 256, 0, stream>>>(ws, a);
-    ransac_refit_kernel<<<g_refit, kScoreThreads, 0, stream>>>(ws, a);
+    ransac_refit_kernel<<<g_refit, kScoreThreads, kRefitSmem, stream>>>(ws, a);
     ransac_finalize_kernel<<<dim3((ws.R + kFinalThreads - 1) / kFinalThreads, ws.B), kFinalThreads, 0, stream>>>(
         ws, a, planes);
     return cudaGetLastError();
