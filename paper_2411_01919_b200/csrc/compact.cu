@@ -165,6 +165,9 @@ compact_scatter_kernel(const float* __restrict__ depth, const int32_t* __restric
     const size_t end = min(beg + (size_t)sub_tile, (size_t)WH);
     const unsigned lt = lanemask_lt();
     int cur = -1, rel = 0, roff = 0;       // cached label, next rank within region, region offset
+    // image coordinates (pu, pv) of this lane's pixel, advanced by 32 pixels
+    // per step (one division per sub-tile instead of a div/mod per step)
+    unsigned pu = (unsigned)((beg + lane) % (unsigned)W), pv = (unsigned)((beg + lane) / (unsigned)W);
     for (size_t i00 = beg; i00 < end; i00 += 32 * kPrefetch) {
         int lraw[kPrefetch];
         float zraw[kPrefetch];
@@ -178,13 +181,10 @@ compact_scatter_kernel(const float* __restrict__ depth, const int32_t* __restric
         for (int u = 0; u < kPrefetch; ++u) {
             const size_t i0 = i00 + u * 32;
             if (i0 >= end) break;
-            const size_t i = i0 + lane;
             const int lab = (valid_depth(zraw[u]) && (unsigned)lraw[u] < (unsigned)R) ? lraw[u] : -1;
-            uint2 pk = make_uint2(0u, 0u);
-            if (lab >= 0) {
-                const unsigned uu = (unsigned)(i % (unsigned)W), vv = (unsigned)(i / (unsigned)W);
-                pk = make_uint2(uu | (vv << 16), __float_as_uint(zraw[u]));
-            }
+            const uint2 pk = make_uint2(pu | (pv << 16), __float_as_uint(zraw[u]));   // used iff lab >= 0
+            pu += 32;
+            while (pu >= (unsigned)W) { pu -= (unsigned)W; ++pv; }
             bool fast = __all_sync(kFull, lab == cur || lab < 0);
             if (!fast) {
                 const int L = __reduce_max_sync(kFull, lab);

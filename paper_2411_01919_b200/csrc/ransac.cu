@@ -493,7 +493,8 @@ ransac_refit_kernel(RansacWorkspace ws, RansacArgs a) {
                         const uint2 q = sp[i];
                         const float3 P = deproject(PackedPoint{q.x, __uint_as_float(q.y)}, a.K.cx, a.K.cy, ifx, ify);
                         const float dist = plane_dist(pl, P);
-                        acc.err += __float2ull_rn(__fmul_rn(fminf(dist, 64.0f), 16777216.0f));
+                        // <= 2^30: a 32-bit conversion (F2I.U32), widened for the sum
+                        acc.err += (unsigned long long)__float2uint_rn(__fmul_rn(fminf(dist, 64.0f), 16777216.0f));
                         if (dist < a.tau) {
                             const double x = (double)P.x - ox, y = (double)P.y - oy, z = (double)P.z - oz;
                             acc.s[0] += x; acc.s[1] += y; acc.s[2] += z;
