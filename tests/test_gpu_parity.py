@@ -210,6 +210,26 @@ def test_ransac_frame_ids_and_batch_invariance(pm):
         assert torch.equal(single.raw, planes.raw[i])
 
 
+def test_ransac_batched_odd_frame_size(pm):
+    """W*H odd: frames 1 and 2 of the batch start 8 B off a 16-B boundary in
+    the compacted point buffer (the refit's bulk copies round the span down /
+    up); every frame must still equal the oracle and its single-frame call."""
+    d, lab, K = scenegen.stair_stream(40, 3, W=333, H=251, n_regions=16)
+    planes = pm.ransac_planes(d.to(DEV), K, lab.to(DEV), 16, 64, 0.01, 5, first_frame_id=40)
+    torch.cuda.synchronize()
+    for i in range(3):
+        ref = oracle.ransac(d[i].numpy(), lab[i].numpy(), K, 16, 64, 0.01, 5, frame_id=40 + i)
+        assert np.array_equal(planes.best_hyp[i].cpu().numpy(), ref["best_hyp"])
+        assert np.array_equal(planes.inliers[i].cpu().numpy(), ref["inliers"])
+        assert np.array_equal(planes.status[i].cpu().numpy(), ref["status"])
+        ok = ref["status"] <= 1
+        assert np.abs(planes.n[i].cpu().numpy()[ok] - ref["n"][ok]).max() <= REFIT_TOL
+        assert np.abs(planes.centroid[i].cpu().numpy()[ok] - ref["centroid"][ok]).max() <= REFIT_TOL
+        single = pm.ransac_planes(d[i].contiguous().to(DEV), K, lab[i].contiguous().to(DEV), 16, 64, 0.01, 5,
+                                  first_frame_id=40 + i)
+        assert torch.equal(single.raw, planes.raw[i])
+
+
 def test_ransac_degenerate_cases(pm):
     K = scenegen.intrinsics_for(64, 48)
     depth = np.full((48, 64), 1.5, np.float32)

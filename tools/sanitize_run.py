@@ -24,5 +24,9 @@ pm.ransac_planes(out, K, lab, 4, 1000, 0.01, 1, sampler=pm.SAMPLER_ENUMERATE, de
 ds, ls, K2 = scenegen.stair_stream(0, 3, 128, 96, 16)
 pm.process_frames(ds.cuda(), ls.cuda(), K2, 0.15, 0.03, 20, 16, 64, 0.01, 7)
 pm.process_frames_host(ds.contiguous(), ls.contiguous(), K2, 0.15, 0.03, 20, 16, 64, 0.01, 7, chunk_frames=2)
+# odd W*H: the second frame's points start 8 B off a 16-B boundary (refit bulk
+# copies round down / up inside the workspace)
+do, lo, K3 = scenegen.stair_stream(0, 3, 333, 251, 16)
+pm.process_frames(do.cuda(), lo.cuda(), K3, 0.15, 0.03, 10, 16, 64, 0.01, 7)
 torch.cuda.synchronize()
 print("sanitize run ok")
