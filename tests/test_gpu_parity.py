@@ -137,9 +137,10 @@ def _ransac_compare(pm, depth_np, labels_np, K, R, H, tau, seed, frame_id=0, sam
         assert np.abs(planes.n.cpu().numpy()[ok] - ref["n"][ok]).max() <= REFIT_TOL
         assert np.abs(planes.d.cpu().numpy()[ok] - ref["d"][ok]).max() <= REFIT_TOL
         assert np.abs(planes.centroid.cpu().numpy()[ok] - ref["centroid"][ok]).max() <= REFIT_TOL
-        sd = planes.sum_dist.cpu().numpy()[ok].astype(np.float64)
-        want = ref["errq"][ok].astype(np.float64) / 2**24
-        assert np.allclose(sd, want, rtol=1e-6, atol=1e-6)
+        # the refit's own fixed-point error sum, exact: sum_dist = f32(errq[best] * 2^-24)
+        sd = planes.sum_dist.cpu().numpy()[ok]
+        want = (ref["errq"][ok].astype(np.float64) / 2**24).astype(np.float32)
+        assert np.array_equal(sd, want)
     return ref
 
 
@@ -228,6 +229,18 @@ def test_ransac_batched_odd_frame_size(pm):
         single = pm.ransac_planes(d[i].contiguous().to(DEV), K, lab[i].contiguous().to(DEV), 16, 64, 0.01, 5,
                                   first_frame_id=40 + i)
         assert torch.equal(single.raw, planes.raw[i])
+
+
+def test_ransac_far_outliers_error_sum(pm):
+    """Depth scattered over 0.3-6 m in every region: most point-plane distances
+    exceed 0.5 m (fixed-point error terms >= 2^23, the refit's second rounding
+    branch) and many exceed the 64 m clamp's scale; counts, winner and the
+    exact error sum must equal the oracle's."""
+    rng = np.random.default_rng(123)
+    K = scenegen.intrinsics_for(96, 72)
+    depth = rng.uniform(0.3, 6.0, (72, 96)).astype(np.float32)
+    labels = (np.arange(96)[None, :] // 24 + 4 * (np.arange(72)[:, None] // 36)).astype(np.int32)
+    _ransac_compare(pm, depth, labels, K, 8, 64, 0.02, 3)
 
 
 def test_ransac_degenerate_cases(pm):
