@@ -310,6 +310,15 @@ PM_DEVINL float3 sobel_normal(const float z[3][3], float u, float v, const AdfPa
     return make_float3(__fmul_rn(mx, inv), __fmul_rn(my, inv), __fmul_rn(mz, inv));
 }
 
+// Fast-path ("hole-free") depth: valid and >= 2^-100.  For such tiles and
+// lambda <= 0.249 an update C + (lambda c) lap >= (1 - 4 lambda c) C >= 0.0036 C
+// stays a positive normal float (lap >= -4C holds after rounding: the
+// neighbour sum is >= 0 and rounding is monotone), so no filtered pixel turns
+// invalid and the normals epilogue may skip its window checks.  Tiles with
+// tiny depths take the checked path, which is exact for every input.
+PM_DEVINL bool fast_depth(float z) { return (__float_as_uint(z) - 0x0D800000u) < (0x7F800000u - 0x0D800000u); }
+constexpr float kNoCheckMaxLambda = 0.249f;
+
 template <int R>
 constexpr size_t pass_smem_bytes() { return sizeof(float) * ((size_t)2 * kSW * (kTH + 2 * R) + kSW); }
 
@@ -367,8 +376,8 @@ adf_pass_kernel(const float* __restrict__ src, float* __restrict__ dst, float* _
             for (int j = 0; j < 4; ++j) in[j] = c0 + j >= b.ix0 && c0 + j < b.ix1;
             for (int sy = b.iy0 + warp; sy < b.iy1; sy += kWarps) {
                 const float4 v = *reinterpret_cast<const float4*>(buf0 + sy * kSW + c0);
-                all_valid &= (valid_depth(v.x) || !in[0]) && (valid_depth(v.y) || !in[1]) &&
-                             (valid_depth(v.z) || !in[2]) && (valid_depth(v.w) || !in[3]);
+                all_valid &= (fast_depth(v.x) || !in[0]) && (fast_depth(v.y) || !in[1]) &&
+                             (fast_depth(v.z) || !in[2]) && (fast_depth(v.w) || !in[3]);
             }
         }
     } else {
@@ -379,7 +388,7 @@ adf_pass_kernel(const float* __restrict__ src, float* __restrict__ dst, float* _
                 const int sx = k * 32 + lane;
                 if (sx >= b.ix0 && sx < b.ix1) {
                     const float v = __ldg(row + sx);
-                    all_valid &= valid_depth(v);
+                    all_valid &= fast_depth(v);
                     buf0[sy * kSW + sx] = v;
                 }
             }
@@ -471,9 +480,11 @@ adf_pass_kernel(const float* __restrict__ src, float* __restrict__ dst, float* _
         using F_ = std::false_type;
         using GEO = std::integral_constant<int, PM_NORMALS_GEOMETRIC>;
         using PRN = std::integral_constant<int, PM_NORMALS_AS_PRINTED>;
-        // hole-free tile: every window is valid (lambda <= 1/4 keeps each
-        // update a convex combination of positive depths, so none turns invalid)
-        const bool nocheck = all_valid && p.lam <= 0.25f;
+        // hole-free tile: every window is valid -- no filtered pixel turns
+        // invalid for lambda <= kNoCheckMaxLambda (fast_depth); at lambda ~ 1/4
+        // a pixel can round to 0 (c = 1 next to much smaller neighbours), so
+        // the windows are checked
+        const bool nocheck = all_valid && (iters == 0 || p.lam <= kNoCheckMaxLambda);
         if (!nrm) quads(F_{}, GEO{});
         else if (p.nmode == PM_NORMALS_AS_PRINTED) { if (nocheck) quads(F_{}, PRN{}); else quads(T_{}, PRN{}); }
         else { if (nocheck) quads(F_{}, GEO{}); else quads(T_{}, GEO{}); }

@@ -101,6 +101,34 @@ def test_adf_special_values_and_edges(pm):
     assert torch.equal(out, c)
 
 
+def test_adf_lambda_quarter_spike_and_tiny_depths(pm):
+    """lambda = 1/4, a spike over much smaller (valid) neighbours: c = 1,
+    lambda c = 1/4 and in f32 the spike rounds to exactly 0 (the neighbour sum
+    is below half an ulp of 4C) -- an invalid filtered pixel, although the
+    diffusion keeps treating it as valid (validity fixed from the input, Q4).
+    The fused normals must mark its windows invalid, i.e. equal the oracle's
+    normals of the GPU's own depth: the unchecked epilogue is only taken when
+    no pixel can turn invalid (lambda <= 0.249, depths >= 2^-100).  Tiny
+    valid depths (< 2^-100) run the checked sweeps."""
+    K = scenegen.intrinsics_for(40, 30)
+    d = np.full((30, 40), 1e-8, np.float32)
+    d[12, 17] = 1.0
+    d[5, 30] = 2.0
+    for iters, T in ((1, 4), (2, 4), (3, 1), (6, 4)):
+        out, nrm = pm.adf_filter(torch.from_numpy(d).to(DEV), K, 0.25, 0.03, iters, iters_per_pass=T)
+        torch.cuda.synchronize()
+        o = out.cpu().numpy()
+        _check_depth(o, d, oracle.adf(d, 0.25, 0.03, iters))
+        if iters == 1:
+            assert o[12, 17] == 0.0 and o[5, 30] == 0.0
+        _check_normals(nrm.cpu().numpy(), oracle.normals(o, K))
+    t = (1.0 + 0.01 * np.random.default_rng(4).standard_normal((30, 40))).astype(np.float32)
+    t[3:9, 4:11] = 1e-35
+    out, _ = pm.adf_filter(torch.from_numpy(t).to(DEV), K, 0.15, 0.03, 9, normals=False)
+    torch.cuda.synchronize()
+    _check_depth(out.cpu().numpy(), t, oracle.adf(t, 0.15, 0.03, 9))
+
+
 def test_adf_bitwise_invariance_to_blocking_and_batch(pm):
     # DESIGN.md §5: identical arithmetic per sweep -> bitwise independent of
     # the iterations fused per pass and of batching
