@@ -283,6 +283,29 @@ def test_ransac_degenerate_cases(pm):
     assert list(ref["status"]) == [2, 3, 2, 0, 2]
 
 
+def test_pipeline_mixed_hole_frames_equal_separate_calls(pm):
+    """pm_process_frames on a batch mixing hole-free frames, frames with
+    dropout holes and a frame with a tiny (< 2^-100) depth equals
+    adf_filter + ransac_planes exactly, for lambda under and over 0.249 and
+    for one and several ADF passes."""
+    d, lab, K = scenegen.stair_stream(7, 5, W=160, H=120, n_regions=16)
+    d = d.clone()
+    rng = np.random.default_rng(11)
+    for i in (1, 3):
+        m = torch.from_numpy(rng.random((120, 160)) < 0.02)
+        d[i][m] = 0.0
+    d[4][60, 80] = 1e-35
+    dev = torch.device(DEV)
+    for lam, iters in ((0.15, 20), (0.25, 9), (0.15, 3)):
+        d_out, nrm, planes = pm.process_frames(d.to(dev), lab.to(dev), K, lam, 0.03, iters, 16, 64, 0.01, 21,
+                                               first_frame_id=7)
+        ref_d, ref_n = pm.adf_filter(d.to(dev), K, lam, 0.03, iters)
+        ref_p = pm.ransac_planes(ref_d, K, lab.to(dev), 16, 64, 0.01, 21, first_frame_id=7)
+        torch.cuda.synchronize()
+        assert torch.equal(d_out, ref_d) and torch.equal(nrm, ref_n)
+        assert torch.equal(planes.raw, ref_p.raw), (lam, iters)
+
+
 def test_pipeline_end_to_end(pm):
     fr = scenegen.make_config("C2")
     dev = torch.device(DEV)
