@@ -310,14 +310,14 @@ PM_DEVINL float3 sobel_normal(const float z[3][3], float u, float v, const AdfPa
     return make_float3(__fmul_rn(mx, inv), __fmul_rn(my, inv), __fmul_rn(mz, inv));
 }
 
-// Fast-path ("hole-free") depth: valid and >= 2^-100.  For such tiles and
-// lambda <= 0.249 an update C + (lambda c) lap >= (1 - 4 lambda c) C >= 0.0036 C
-// stays a positive normal float (lap >= -4C holds after rounding: the
-// neighbour sum is >= 0 and rounding is monotone), so no filtered pixel turns
-// invalid and the normals epilogue may skip its window checks.  Tiles with
-// tiny depths take the checked path, which is exact for every input.
-PM_DEVINL bool fast_depth(float z) { return (__float_as_uint(z) - 0x0D800000u) < (0x7F800000u - 0x0D800000u); }
-constexpr float kNoCheckMaxLambda = 0.249f;
+// Fast-path ("hole-free") depth: valid and in [2^-100, 2^100).  For such
+// tiles and lambda <= kNoCheckMaxLambda (internal.h) an update
+// C + (lambda c) lap >= (1 - 4 lambda c) C >= 0.0036 C stays a positive normal
+// float (lap >= -4C holds after rounding: the neighbour sum is >= 0, finite,
+// and rounding is monotone), so no filtered pixel turns invalid: the normals
+// epilogue may skip its window checks, and pm_process_frames' compaction
+// count its depth reads.  Other tiles take the checked path.
+PM_DEVINL bool fast_depth(float z) { return (__float_as_uint(z) - 0x0D800000u) < (0x71800000u - 0x0D800000u); }
 
 template <int R>
 constexpr size_t pass_smem_bytes() { return sizeof(float) * ((size_t)2 * kSW * (kTH + 2 * R) + kSW); }

@@ -75,7 +75,7 @@ pm_status adf_impl(const float* in, float* out, int32_t W, int32_t H, int32_t B,
 pm_status ransac_impl(const float* depth, int32_t W, int32_t H, int32_t B, uint32_t first_frame,
                       const pm_intrinsics* K, const int32_t* labels, int32_t R, int32_t n_hyp,
                       float tau, uint64_t seed, pm_plane* planes, void* ws, size_t ws_bytes,
-                      const pm_ransac_options* opt, cudaStream_t stream) {
+                      const pm_ransac_options* opt, cudaStream_t stream, const int* depth_all_valid = nullptr) {
     if (!depth || !labels || !dims_ok(W, H, B) || !intrinsics_ok(K)) return PM_ERR_INVALID_ARGUMENT;
     if (R < 0 || R > 65536 || n_hyp < 1 || n_hyp > 4096 || !finite_pos(tau)) return PM_ERR_INVALID_ARGUMENT;
     if (R > 0 && !planes) return PM_ERR_INVALID_ARGUMENT;
@@ -95,7 +95,7 @@ pm_status ransac_impl(const float* depth, int32_t W, int32_t H, int32_t B, uint3
     if (!ws || ws_bytes < need || !aligned256(ws)) return PM_ERR_WORKSPACE;
     if (cudaError_t e = setup(); e != cudaSuccess) return PM_ERR_CUDA;
     const pm::RansacWorkspace L = pm::ransac_workspace_layout(ws, W, H, R, n_hyp, B);
-    cudaError_t e = pm::compact_run(depth, labels, L, stream);
+    cudaError_t e = pm::compact_run(depth, labels, L, stream, depth_all_valid);
     if (e != cudaSuccess) return PM_ERR_CUDA;
     pm::RansacArgs a;
     a.K = *K;
@@ -214,8 +214,21 @@ PM_API pm_status pm_process_frames(const float* depth_in, const int32_t* region_
     pm_status s = adf_impl(depth_in, depth_out, W, H, n_frames, K, lambda, kappa, iters, normals_out, workspace,
                            ws_bytes, 0, PM_ADF_ALG1, PM_NORMALS_GEOMETRIC, PM_ADF_ENGINE_AUTO, (cudaStream_t)stream);
     if (s != PM_OK) return s;
+    // The ADF's per-frame flags (written by its first pass when it runs more
+    // than one; 0 = every input depth valid and in [2^-100, 2^100)) say which
+    // filtered frames hold valid depths only (lambda <= kNoCheckMaxLambda,
+    // adf.cu fast_depth): their compaction count skips the depth reads.  The
+    // flags sit in the ping-pong region, inside the compaction's point buffer
+    // (checked: not in the histogram it clears first), which is written only
+    // after the count.
+    const int T = pm::adf_default_iters_per_pass();
+    const size_t flags_off = pm::adf_flags_offset(W, H, n_frames);
+    const bool flags_live = iters > T && lambda <= pm::kNoCheckMaxLambda &&
+                            flags_off + sizeof(int) * (size_t)n_frames <= sizeof(uint64_t) * (size_t)n_frames * W * H;
+    const int* fast =
+        flags_live ? reinterpret_cast<const int*>(static_cast<const char*>(workspace) + flags_off) : nullptr;
     return ransac_impl(depth_out, W, H, n_frames, first_frame_id, K, region_labels, n_regions, n_hyp,
-                       inlier_thresh, seed, planes_out, workspace, ws_bytes, nullptr, (cudaStream_t)stream);
+                       inlier_thresh, seed, planes_out, workspace, ws_bytes, nullptr, (cudaStream_t)stream, fast);
 }
 
 PM_API int32_t pm_pipeline_kernel_launches(int32_t iters, int32_t n_regions) {

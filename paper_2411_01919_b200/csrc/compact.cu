@@ -82,6 +82,69 @@ compact_count_kernel(const float* __restrict__ depth, const int32_t* __restrict_
     if (cur >= 0 && lane == 0) h[(size_t)cur * n_sub + st] += cnt;
 }
 
+// Count with a run cache per LANE (R <= kLaneCountMaxR): lane l walks pixels
+// l, l+32, ... of the warp's sub-tile and flushes its (label, run length) into
+// the warp's shared-memory histogram row only when its label changes, so a
+// 32-pixel step costs ~8-12 instructions (the warp-vote walk above: ~37).
+// The warp then writes its nonzero (region, sub-tile) entries -- the same
+// owner-exclusive hist the scatter reads.  NEED_Z = false: the frame is known
+// to hold valid depths only (depth_all_valid[f] == 0) and only labels are read.
+constexpr int kLaneCountMaxR = 256;
+template <bool NEED_Z>
+PM_DEVINL void count_lane_walk(const float* __restrict__ d, const int32_t* __restrict__ l, unsigned beg, unsigned end,
+                               int R, int lane, int* __restrict__ row) {
+    int cur = -1, cnt = 0;
+    for (unsigned i00 = beg; i00 < end; i00 += 32 * kPrefetch) {
+        int lraw[kPrefetch];
+        float zraw[kPrefetch];
+#pragma unroll
+        for (int u = 0; u < kPrefetch; ++u) {        // all loads of kPrefetch steps in flight
+            const unsigned i = i00 + u * 32 + lane;
+            lraw[u] = i < end ? __ldg(l + i) : -1;
+            if (NEED_Z) zraw[u] = i < end ? __ldg(d + i) : 0.0f;
+        }
+#pragma unroll
+        for (int u = 0; u < kPrefetch; ++u) {
+            const int lab = ((!NEED_Z || valid_depth(zraw[u])) && (unsigned)lraw[u] < (unsigned)R) ? lraw[u] : -1;
+            if (lab >= 0) {
+                if (lab != cur) {                      // rare: a region boundary in this lane's column
+                    if (cur >= 0) atomicAdd(row + cur, cnt);
+                    cur = lab;
+                    cnt = 0;
+                }
+                ++cnt;
+            }
+        }
+    }
+    if (cur >= 0) atomicAdd(row + cur, cnt);
+}
+
+__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+compact_count_lane_kernel(const float* __restrict__ depth, const int32_t* __restrict__ labels,
+                          int WH, int R, int sub_tile, int n_sub, int32_t* __restrict__ hist,
+                          const int* __restrict__ depth_all_valid) {
+    __shared__ int s_h[kWarpsPerBlock][kLaneCountMaxR];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int st = blockIdx.x * kWarpsPerBlock + w;
+    if (st >= n_sub) return;                     // warp-level only: no block barrier below
+    const size_t f = blockIdx.y;
+    int* row = s_h[w];
+    for (int r = lane; r < R; r += 32) row[r] = 0;
+    __syncwarp();
+    const unsigned beg = (unsigned)st * (unsigned)sub_tile;
+    const unsigned end = min(beg + (unsigned)sub_tile, (unsigned)WH);
+    const float* d = depth + f * WH;
+    const int32_t* l = labels + f * WH;
+    if (depth_all_valid == nullptr || depth_all_valid[f] != 0) count_lane_walk<true>(d, l, beg, end, R, lane, row);
+    else count_lane_walk<false>(d, l, beg, end, R, lane, row);
+    __syncwarp();
+    int32_t* h = hist + f * (size_t)R * n_sub;
+    for (int r = lane; r < R; r += 32) {
+        const int v = row[r];
+        if (v) h[(size_t)r * n_sub + st] = v;
+    }
+}
+
 // one warp per (frame, region): exclusive prefix over sub-tiles, total count
 __global__ void __launch_bounds__(kWarpsPerBlock * 32)
 compact_scan_kernel(int R, int n_sub, int32_t* __restrict__ hist, int32_t* __restrict__ region_cnt) {
@@ -223,13 +286,17 @@ compact_scatter_kernel(const float* __restrict__ depth, const int32_t* __restric
 }  // namespace
 
 cudaError_t compact_run(const float* depth, const int32_t* labels, const RansacWorkspace& ws,
-                        cudaStream_t stream) {
+                        cudaStream_t stream, const int* depth_all_valid) {
     const int WH = ws.W * ws.H;
     cudaError_t e = cudaMemsetAsync(ws.hist, 0, sizeof(int32_t) * (size_t)ws.B * ws.R * ws.n_sub, stream);
     if (e != cudaSuccess) return e;
     const dim3 blk(kWarpsPerBlock * 32);
     const dim3 g_tiles((ws.n_sub + kWarpsPerBlock - 1) / kWarpsPerBlock, ws.B);
-    compact_count_kernel<<<g_tiles, blk, 0, stream>>>(depth, labels, WH, ws.R, ws.sub_tile, ws.n_sub, ws.hist);
+    if (ws.R <= kLaneCountMaxR && (long long)ws.W * ws.H < (1ll << 31))
+        compact_count_lane_kernel<<<g_tiles, blk, 0, stream>>>(depth, labels, WH, ws.R, ws.sub_tile, ws.n_sub,
+                                                               ws.hist, depth_all_valid);
+    else
+        compact_count_kernel<<<g_tiles, blk, 0, stream>>>(depth, labels, WH, ws.R, ws.sub_tile, ws.n_sub, ws.hist);
     const dim3 g_regions((ws.R + kWarpsPerBlock - 1) / kWarpsPerBlock, ws.B);
     compact_scan_kernel<<<g_regions, blk, 0, stream>>>(ws.R, ws.n_sub, ws.hist, ws.region_cnt);
     compact_offsets_kernel<<<ws.B, 1024, 0, stream>>>(ws.R, ws.region_cnt, ws.region_off);

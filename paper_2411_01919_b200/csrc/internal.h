@@ -13,6 +13,9 @@ cudaError_t adf_setup_attributes();
 int adf_default_iters_per_pass();
 // byte offset of the per-frame validity flags inside the adf workspace
 size_t adf_flags_offset(int W, int H, int B);
+// lambda bound under which a frame whose ADF flag is 0 (every input depth
+// valid and in [2^-100, 2^100), adf.cu fast_depth) filters to valid depths only
+constexpr float kNoCheckMaxLambda = 0.249f;
 // in -> out (B frames); ws: B*H*W floats (used when >= 2 passes); normals nullable.
 cudaError_t adf_run(const float* in, float* out, float* normals, float* ws, int W, int H, int B,
                     const pm_intrinsics* K, float lam, float kappa, int iters, int iters_per_pass,
@@ -54,8 +57,11 @@ struct RansacWorkspace {
 // Carve `base` (nullable: sizing only) into the ransac workspace.
 RansacWorkspace ransac_workspace_layout(void* base, int W, int H, int R, int n_hyp, int B);
 
+// depth_all_valid (nullable): per-frame flags, 0 = every depth of the frame is
+// known valid (pm_process_frames passes the ADF's fast-depth flags), so the
+// count reads labels only
 cudaError_t compact_run(const float* depth, const int32_t* labels, const RansacWorkspace& ws,
-                        cudaStream_t stream);
+                        cudaStream_t stream, const int* depth_all_valid = nullptr);
 
 struct RansacArgs {
     pm_intrinsics K;
