@@ -9,7 +9,10 @@
 //             running count) in registers and touches memory only when the
 //             label changes; a step with several labels falls back to
 //             __match_any_sync groups.  hist entries are owned by one warp:
-//             no atomics, no ordering dependence.
+//             no atomics, no ordering dependence.  For R <= 256 the
+//             count_lane variant keeps the run cache per lane instead (shared
+//             histogram row per warp), and skips the depth reads for frames
+//             known to hold valid depths only (pm_process_frames).
 //   scan    : per (frame, region) exclusive prefix over sub-tiles -> counts;
 //             per frame exclusive prefix over regions -> region offsets.
 //   scatter : the same warp walk, writing packed (u, v, z) points to
