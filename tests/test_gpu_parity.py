@@ -306,6 +306,54 @@ def test_pipeline_mixed_hole_frames_equal_separate_calls(pm):
         assert torch.equal(planes.raw, ref_p.raw), (lam, iters)
 
 
+@pytest.mark.parametrize("W,H", [(3, 3), (5, 4), (7, 33), (31, 9), (33, 3)])
+def test_pipeline_tiny_frames(pm, W, H):
+    """Frames at and just above the minimum size (3x3) and narrower than a
+    warp: partial tiles everywhere, the compaction's per-step coordinate
+    advance wrapping several rows at once (W < 32), one to few points per
+    region.  Depth, normals and planes of pm_process_frames vs the oracle,
+    batched frames vs single-frame calls."""
+    rng = np.random.default_rng(W * 100 + H)
+    K = scenegen.intrinsics_for(W, H)
+    B, R = 3, 4
+    d = (1.0 + 0.3 * rng.random((B, H, W))).astype(np.float32)
+    d[1, 0, 0] = 0.0
+    lab = rng.integers(-1, R, (B, H, W)).astype(np.int32)
+    dev = torch.device(DEV)
+    for iters in (0, 3, 9):
+        d_out, nrm, planes = pm.process_frames(torch.from_numpy(d).to(dev), torch.from_numpy(lab).to(dev), K, 0.15,
+                                               0.03, iters, R, 16, 0.05, 3, first_frame_id=2)
+        torch.cuda.synchronize()
+        for i in range(B):
+            o = d_out[i].cpu().numpy()
+            _check_depth(o, d[i], oracle.adf(d[i], 0.15, 0.03, iters))
+            _check_normals(nrm[i].cpu().numpy(), oracle.normals(o, K))
+            ref = oracle.ransac(o, lab[i], K, R, 16, 0.05, 3, frame_id=2 + i)
+            assert np.array_equal(planes.n_points[i].cpu().numpy(), ref["n_points"])
+            assert np.array_equal(planes.best_hyp[i].cpu().numpy(), ref["best_hyp"])
+            assert np.array_equal(planes.inliers[i].cpu().numpy(), ref["inliers"])
+            assert np.array_equal(planes.status[i].cpu().numpy(), ref["status"])
+
+
+def test_pipeline_no_regions_and_unlabelled(pm):
+    """n_regions = 0 (RANSAC skipped: depth and normals still produced) and
+    every label -1 (every region TOO_FEW with 0 points)."""
+    fr = scenegen.make_config("C1n")
+    dev = torch.device(DEV)
+    d = fr["depth"].to(dev)
+    d_out, nrm, planes = pm.process_frames(d, fr["labels"].to(dev), fr["K"], fr["lam"], fr["kappa"], fr["iters"],
+                                           0, fr["n_hyp"], fr["tau"], fr["seed"])
+    ref_d, ref_n = pm.adf_filter(d, fr["K"], fr["lam"], fr["kappa"], fr["iters"])
+    torch.cuda.synchronize()
+    assert torch.equal(d_out, ref_d) and torch.equal(nrm, ref_n)
+    none = torch.full_like(fr["labels"], -1).to(dev)
+    _, _, planes = pm.process_frames(d, none, fr["K"], fr["lam"], fr["kappa"], fr["iters"], 4, fr["n_hyp"],
+                                     fr["tau"], fr["seed"])
+    torch.cuda.synchronize()
+    assert planes.n_points.cpu().tolist() == [0, 0, 0, 0]
+    assert planes.status.cpu().tolist() == [2, 2, 2, 2]
+
+
 def test_pipeline_end_to_end(pm):
     fr = scenegen.make_config("C2")
     dev = torch.device(DEV)
