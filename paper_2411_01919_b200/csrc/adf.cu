@@ -419,13 +419,20 @@ adf_pass_kernel(const float* __restrict__ src, float* __restrict__ dst, float* _
             done = true;
         }
     }
-    for (int t = 1; !done && t <= iters; ++t) {
-#define PM_SWEEP(FN, CK) FN<SH, PAD, CK, DIV>(cur, nxt, t, b, p)
-        if (pairs) { if (all_valid) PM_SWEEP(sweep_pairs, false); else PM_SWEEP(sweep_pairs, true); }
-        else { if (all_valid) PM_SWEEP(sweep, false); else PM_SWEEP(sweep, true); }
-#undef PM_SWEEP
-        __syncthreads();
-        float* tmp = cur; cur = nxt; nxt = tmp;
+    // generic tiles: one sweep loop per variant (the variant test outside the
+    // loop lets the sweep-invariant column setup be hoisted out of it)
+    auto sweeps = [&](auto FN) {
+        for (int t = 1; t <= iters; ++t) {
+            FN(t);
+            __syncthreads();
+            float* tmp = cur; cur = nxt; nxt = tmp;
+        }
+    };
+    if (!done) {
+#define PM_SWEEPS(FN, CK) sweeps([&](int t) { FN<SH, PAD, CK, DIV>(cur, nxt, t, b, p); })
+        if (pairs) { if (all_valid) PM_SWEEPS(sweep_pairs, false); else PM_SWEEPS(sweep_pairs, true); }
+        else { if (all_valid) PM_SWEEPS(sweep, false); else PM_SWEEPS(sweep, true); }
+#undef PM_SWEEPS
     }
 
     // write the tile (and its normals).  Rows of float4 quads when W % 4 == 0
