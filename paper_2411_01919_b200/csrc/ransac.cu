@@ -149,6 +149,21 @@ struct Chunk {
     int s, e, r0;
 };
 
+// max{r < R : off[r] <= s} for nondecreasing off[] with off[0] = 0 <= s, by
+// one full warp: a 32-ary search (every lane probes one offset per level; the
+// ballot is a prefix), log32(R) dependent loads instead of log2(R).
+PM_DEVINL int first_region(const int32_t* off, int R, int s, int lane) {
+    int r0 = 0;
+    for (int hi = R; hi - r0 > 1;) {
+        const int step = (hi - r0 + 31) >> 5;
+        const int p = r0 + lane * step;
+        const unsigned le = __ballot_sync(kFull, lane == 0 || (p < hi && off[p] <= s));
+        r0 += (31 - __clz(le)) * step;
+        hi = min(hi, r0 + step);
+    }
+    return r0;
+}
+
 PM_DEVINL bool stage_chunk(const RansacWorkspace& ws, const RansacArgs& a, size_t f, float4* sp, int* s_r0,
                            Chunk& ck) {
     // points per CTA: kScoreChunk
@@ -165,13 +180,9 @@ PM_DEVINL bool stage_chunk(const RansacWorkspace& ws, const RansacArgs& a, size_
         const float3 P = deproject(PackedPoint{q.x, __uint_as_float(q.y)}, a.K.cx, a.K.cy, ifx, ify);
         sp[i] = make_float4(P.x, P.y, P.z, 0.f);
     }
-    if (threadIdx.x == 0) {                 // region with off[r] <= s < off[r+1]
-        int lo = 0, hi = R;                 // invariant: off[lo] <= s, off[hi] = total > s
-        while (hi - lo > 1) {
-            const int mid = (lo + hi) >> 1;
-            if (off[mid] <= ck.s) lo = mid; else hi = mid;
-        }
-        *s_r0 = lo;
+    if (threadIdx.x < 32) {                 // region with off[r] <= s < off[r+1]
+        const int r0 = first_region(off, R, ck.s, threadIdx.x);
+        if (threadIdx.x == 0) *s_r0 = r0;
     }
     __syncthreads();
     ck.r0 = *s_r0;
@@ -428,7 +439,6 @@ __global__ void __launch_bounds__(kScoreThreads)
 ransac_refit_kernel(RansacWorkspace ws, RansacArgs a) {
     extern __shared__ __align__(16) uint2 s_pts[];            // [warp][half][kHalfSlot]
     __shared__ __align__(8) uint64_t s_bar[kRefitWarps][2];
-    __shared__ int s_r0;
     const size_t f = blockIdx.y;
     const int R = ws.R, HP = ws.n_hyp_pad;
     const int32_t* off = ws.region_off + f * (size_t)(R + 1);
@@ -460,26 +470,46 @@ ransac_refit_kernel(RansacWorkspace ws, RansacArgs a) {
             mbar_arrive_expect_tx(&s_bar[w][1], bytes);
             bulk_load_g2s(sb1, pts + hs1 - sh1, bytes, &s_bar[w][1]);
         }
-        int lo = 0, hi = R;
-        while (hi - lo > 1) {
-            const int mid = (lo + hi) >> 1;
-            if (off[mid] <= cs) lo = mid; else hi = mid;
-        }
-        if (w == 0) s_r0 = lo;
     }
-    __syncthreads();          // region start and the mbarrier inits visible to every warp
+    const int r0 = first_region(off, R, cs, lane);          // first region of the chunk
+    // lane j prefetches region r0 + j (offsets, winner, winner's plane, first
+    // point) in two rounds of independent loads; the region loop below takes
+    // them by shuffle instead of four dependent loads per region
+    const int rl = r0 + lane;
+    const int offL = rl <= R ? off[rl] : 0;
+    const int bestL = rl < R ? ws.best[f * R + rl] : -1;
+    float4 plL = make_float4(0.f, 0.f, 0.f, 0.f);
+    uint2 q0L = make_uint2(0u, 0u);
+    if (bestL >= 0 && offL < ce) {                           // best >= 0: >= 3 points
+        plL = ws.planes[(f * R + rl) * HP + bestL];
+        q0L = pts[offL];
+    }
+    __syncthreads();          // the mbarrier inits visible before any wait
     const float ifx = 1.0f / a.K.fx, ify = 1.0f / a.K.fy;
     int ready = 0;                                           // bit h: half h waited on
-    for (int r = s_r0; r < R && off[r] < ce; ++r) {
-        const int lo = max(cs, off[r]), hi = min(ce, off[r + 1]);
+    for (int r = r0; r < R; ++r) {
+        const int j = r - r0;                                // warp-uniform
+        const bool pre = j < 31;
+        const int o0 = pre ? __shfl_sync(kFull, offL, j) : off[r];
+        if (o0 >= ce) break;
+        const int o1 = pre ? __shfl_sync(kFull, offL, j + 1) : off[r + 1];
+        const int lo = max(cs, o0), hi = min(ce, o1);
         if (hi <= lo) continue;
-        const int best = ws.best[f * R + r];
+        const int best = pre ? __shfl_sync(kFull, bestL, j) : ws.best[f * R + r];
         if (best >= 0) {
             const int a0 = max(lo, wlo), a1 = min(hi, whi);
             Sums acc = {};
             if (a0 < a1) {                                    // warp-uniform
-                const float4 pl = ws.planes[(f * R + r) * HP + best];
-                const uint2 q0 = pts[off[r]];
+                float4 pl;
+                uint2 q0;
+                if (pre) {
+                    pl = make_float4(__shfl_sync(kFull, plL.x, j), __shfl_sync(kFull, plL.y, j),
+                                     __shfl_sync(kFull, plL.z, j), __shfl_sync(kFull, plL.w, j));
+                    q0 = make_uint2(__shfl_sync(kFull, q0L.x, j), __shfl_sync(kFull, q0L.y, j));
+                } else {
+                    pl = ws.planes[(f * R + r) * HP + best];
+                    q0 = pts[o0];
+                }
                 const float3 o3 = deproject(PackedPoint{q0.x, __uint_as_float(q0.y)}, a.K.cx, a.K.cy, ifx, ify);
                 const double ox = o3.x, oy = o3.y, oz = o3.z;
 #pragma unroll 1

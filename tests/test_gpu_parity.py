@@ -283,6 +283,22 @@ def test_ransac_degenerate_cases(pm):
     assert list(ref["status"]) == [2, 3, 2, 0, 2]
 
 
+def test_ransac_many_regions_per_chunk(pm):
+    """Hundreds of 4x4-pixel regions (some empty, some with 1-2 points) so one
+    8192-point score / refit chunk meets far more than 32 regions: the refit's
+    per-region prefetch (first 31 regions of a chunk by shuffle, the rest by
+    direct loads) and the 32-ary first-region search, bit-exact vs the oracle."""
+    fr = scenegen.make_config("C2", W=128, H=96)
+    d = fr["depth"].numpy()
+    v, u = np.mgrid[0:96, 0:128]
+    lab = ((v // 4) * 32 + u // 4).astype(np.int32)          # 768 regions of 16 px
+    lab[(lab % 7) == 3] = -1                                  # empty regions
+    lab[((lab % 11) == 5) & ((u % 4) > 0)] = -1               # 4-point regions
+    lab[((lab % 13) == 6) & ((u % 4) + (v % 4) > 0)] = -1     # 1-point regions
+    ref = _ransac_compare(pm, d, lab, fr["K"], 768, 16, fr["tau"], 3)
+    assert (ref["n_points"] == 0).any() and (ref["n_points"] == 1).any() and (ref["status"] == 0).any()
+
+
 def test_pipeline_mixed_hole_frames_equal_separate_calls(pm):
     """pm_process_frames on a batch mixing hole-free frames, frames with
     dropout holes and a frame with a tiny (< 2^-100) depth equals
