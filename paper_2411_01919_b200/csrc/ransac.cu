@@ -194,6 +194,14 @@ PM_DEVINL void count_lt(int& c, float a, float b) {
     asm("{\n.reg .pred p;\nsetp.lt.f32 p, %1, %2;\n@p add.s32 %0, %0, 1;\n}" : "+r"(c) : "f"(a), "f"(b));
 }
 
+// pairs j with bit (j mod 4) set count on the FMA pipe (FSET + FADD2), the
+// others on the ALU pipe (FSETP + predicated IADD).  Measured on the bench
+// step (tools/ab_fadd_mask.sh): mask 0 (all on the ALU pipe) 3.031 ms,
+// 5 (even pairs) 3.048, 1: 3.076, 7: 3.112, 15: 3.134 ms RANSAC stage.
+#ifndef PM_SCORE_FADD_MASK
+#define PM_SCORE_FADD_MASK 0
+#endif
+
 // Packed-pair scoring (two hypotheses per FFMA2 chain) for even K without the
 // error sum, reading the plane pairs the hyp kernel lays out (ws.pairs).
 template <int K, int L, bool WITH_ERR>
@@ -285,9 +293,9 @@ ransac_score_kernel(RansacWorkspace ws, RansacArgs a) {
                     asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(d) : "l"(Y[j]), "l"(py));
                     asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(d) : "l"(Z[j]), "l"(pz));
                     const float2 df = f2up(d);
-                    if (j & 1) {
-                        // odd pairs count on the ALU pipe (FSETP + predicated IADD),
-                        // even pairs on the FMA pipe (FADD2): both pipes stay busy
+                    if (!((PM_SCORE_FADD_MASK >> (j & 3)) & 1)) {
+                        // ALU-pipe count (FSETP + predicated IADD): the FMA pipe
+                        // keeps the three FFMA2 of the distance
                         count_lt(c[2 * j], fabsf(df.x), tau);
                         count_lt(c[2 * j + 1], fabsf(df.y), tau);
                     } else {
@@ -299,7 +307,8 @@ ransac_score_kernel(RansacWorkspace ws, RansacArgs a) {
                 }
             }
 #pragma unroll
-            for (int j = 0; j < K2; j += 2) {
+            for (int j = 0; j < K2; ++j) {
+                if (!((PM_SCORE_FADD_MASK >> (j & 3)) & 1)) continue;
                 const float2 a2 = f2up(acc[j]);
                 c[2 * j] = (int)a2.x;
                 c[2 * j + 1] = (int)a2.y;
