@@ -282,7 +282,7 @@ ransac_score_kernel(RansacWorkspace ws, RansacArgs a) {
             uint64_t acc[K2];
 #pragma unroll
             for (int j = 0; j < K2; ++j) acc[j] = 0ull;
-#pragma unroll 4
+#pragma unroll 8
             for (int i = lo + g; i < hi; i += G) {
                 const float4 p4 = sp[i];
                 const uint64_t px = f2pk(f2s(p4.x)), py = f2pk(f2s(p4.y)), pz = f2pk(f2s(p4.z));
