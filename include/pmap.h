@@ -117,12 +117,13 @@ PM_API size_t pm_adf_workspace_bytes(int32_t W, int32_t H, int32_t n_frames);
  *   PM_NORMALS_AS_PRINTED  Eq. 2 literally: n = -K^-1 [Gx, Gy, 1]^T, normalised */
 enum { PM_ADF_ALG1 = 0, PM_ADF_DIVERGENCE = 1 };
 enum { PM_NORMALS_GEOMETRIC = 0, PM_NORMALS_AS_PRINTED = 1 };
-/* engine: AUTO = TILED (the faster engine on B200);
- * TILED = shared-memory tiles, iters_per_pass sweeps (default 4) per HBM pass;
- * STREAM = the wavefront kernel: one walk down the frame per pass carrying up
- * to 20 sweeps at once (no y halo, one HBM pass), falls back to TILED when W
- * is odd.  Both engines give bitwise identical results. */
-enum { PM_ADF_ENGINE_AUTO = 0, PM_ADF_ENGINE_TILED = 1, PM_ADF_ENGINE_STREAM = 2 };
+/* engine: AUTO = TILED (the faster engine on B200, DESIGN.md §11);
+ * REG = register-resident tiles (csrc/adf_reg.cu; W % 4 == 0, H >= 128,
+ * 16-B aligned depth), falls back to TILED where it does not apply;
+ * TILED = shared-memory tiles, iters_per_pass sweeps (default 4) per HBM pass.
+ * Both engines give bitwise identical results.  (Value 2, a wavefront engine
+ * of round 1, was removed: 2.6x slower than TILED.) */
+enum { PM_ADF_ENGINE_AUTO = 0, PM_ADF_ENGINE_TILED = 1, PM_ADF_ENGINE_REG = 3 };
 typedef struct {
     int32_t iters_per_pass;   /* sweeps per HBM pass (1..16); 0 = engine default */
     int32_t scheme;           /* PM_ADF_*        */

@@ -1,6 +1,6 @@
 // api.cu — the C ABI of include/pmap.h: argument validation, workspace
 // carving and launch sequencing on the caller's stream.  No allocation on the
-// hot path; the only global state is the one-time kernel attribute setup.
+// hot path; the only global state is the one-time (per device) kernel attribute setup.
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
@@ -14,16 +14,23 @@ namespace {
 
 constexpr int32_t kVersion = 100;   // 0.1.0
 
-std::once_flag g_once;
-cudaError_t g_setup_err = cudaSuccess;
+// Kernel attributes (> 48 KB dynamic shared memory) are per device context:
+// set once per device, on first use from any thread.
+constexpr int kMaxDevices = 64;
+std::once_flag g_once[kMaxDevices];
+cudaError_t g_setup_err[kMaxDevices];
 
 cudaError_t setup() {
-    std::call_once(g_once, [] {
-        g_setup_err = pm::adf_setup_attributes();
-        if (g_setup_err == cudaSuccess) g_setup_err = pm::adf_stream_setup_attributes();
-        if (g_setup_err == cudaSuccess) g_setup_err = pm::ransac_setup_attributes();
+    int dev = 0;
+    if (cudaError_t e = cudaGetDevice(&dev); e != cudaSuccess) return e;
+    if (dev < 0 || dev >= kMaxDevices) return cudaErrorInvalidDevice;
+    std::call_once(g_once[dev], [dev] {
+        cudaError_t e = pm::adf_setup_attributes();
+        if (e == cudaSuccess) e = pm::adf_reg_setup_attributes();
+        if (e == cudaSuccess) e = pm::ransac_setup_attributes();
+        g_setup_err[dev] = e;
     });
-    return g_setup_err;
+    return g_setup_err[dev];
 }
 
 bool finite_pos(float x) { return x > 0.0f && isfinite(x); }
@@ -49,7 +56,7 @@ pm_status cuda_status(cudaError_t e) { return e == cudaSuccess ? PM_OK : PM_ERR_
 pm_status adf_impl(const float* in, float* out, int32_t W, int32_t H, int32_t B, const pm_intrinsics* K,
                    float lam, float kappa, int32_t iters, float* normals, void* ws, size_t ws_bytes,
                    int32_t iters_per_pass, int32_t scheme, int32_t nmode, int32_t engine, cudaStream_t stream) {
-    if (engine != PM_ADF_ENGINE_AUTO && engine != PM_ADF_ENGINE_TILED && engine != PM_ADF_ENGINE_STREAM)
+    if (engine != PM_ADF_ENGINE_AUTO && engine != PM_ADF_ENGINE_TILED && engine != PM_ADF_ENGINE_REG)
         return PM_ERR_INVALID_ARGUMENT;
     if (scheme != PM_ADF_ALG1 && scheme != PM_ADF_DIVERGENCE) return PM_ERR_INVALID_ARGUMENT;
     if (nmode != PM_NORMALS_GEOMETRIC && nmode != PM_NORMALS_AS_PRINTED) return PM_ERR_INVALID_ARGUMENT;
@@ -61,8 +68,7 @@ pm_status adf_impl(const float* in, float* out, int32_t W, int32_t H, int32_t B,
     if (normals && (overlap(normals, 3 * bytes, in, bytes) || overlap(normals, 3 * bytes, out, bytes)))
         return PM_ERR_INVALID_ARGUMENT;
     if (iters_per_pass < 0 || iters_per_pass > 16) return PM_ERR_INVALID_ARGUMENT;   // 16 = adf.cu kMaxItersPerPass
-    // the ping-pong workspace is required whenever a pass of the tiled engine
-    // (the fallback of the wavefront engine) would not hold all the sweeps
+    // the ping-pong workspace is required whenever one pass does not hold all the sweeps
     const int T = iters_per_pass > 0 ? iters_per_pass : pm::adf_default_iters_per_pass();
     const bool needs_ws = iters > T;
     if (needs_ws && (!ws || ws_bytes < pm_adf_workspace_bytes(W, H, B) || !aligned256(ws))) return PM_ERR_WORKSPACE;

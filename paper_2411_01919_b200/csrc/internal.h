@@ -20,18 +20,8 @@ constexpr float kNoCheckMaxLambda = 0.249f;
 cudaError_t adf_run(const float* in, float* out, float* normals, float* ws, int W, int H, int B,
                     const pm_intrinsics* K, float lam, float kappa, int iters, int iters_per_pass,
                     int scheme, int nmode, int engine, cudaStream_t stream);
-// ---- adf_stream.cu (wavefront kernel: all sweeps of a pass in one walk)
-struct AdfStreamParams {
-    float kc, l2lam, kd, lam;
-    float fx, fy, cx, cy, ifx, ify;
-    int scheme, nmode;
-};
-cudaError_t adf_stream_setup_attributes();
-int adf_stream_max_levels();
-bool adf_stream_applicable(int W, int H, int levels);
-cudaError_t adf_stream_pass(const float* src, float* dst, float* normals, int W, int H, int B, int levels,
-                            const AdfStreamParams& p, cudaStream_t stream);
-
+// ---- adf_reg.cu (register-tile engine; the pass launcher is declared in adf_cell.cuh)
+cudaError_t adf_reg_setup_attributes();
 cudaError_t normals_run(const float* depth, float* normals, int W, int H, int B,
                         const pm_intrinsics* K, int nmode, cudaStream_t stream);
 

@@ -176,3 +176,99 @@ def test_map_capacity_overflow_leaves_map_untouched():
     with pytest.raises(pm.PMError):
         M.merge_frame(_table(rows), IDENT)
     assert M.count.value == 0 and M.filter.x == 0.0
+
+
+# ------------------------------------------------------------------ oracle pins
+# The checks below run on oracle/mapman.py ALONE (no product code), so a
+# pose-convention mistake shared by the oracle and csrc/mapman.cpp fails here.
+def test_oracle_to_world_closed_forms():
+    # yaw +90 deg about world z (n_w = R n, c_w = R c + t; the pose
+    # is the row-major 4x4 camera-to-world matrix): camera x -> world y,
+    # camera y -> world -x, camera z -> world z
+    P = _pose(math.pi / 2, (10.0, 20.0, 30.0))
+    nw, cw = orc.to_world([1.0, 0.0, 0.0], [1.0, 2.0, 3.0], P)
+    assert np.allclose(nw, [0.0, 1.0, 0.0], atol=1e-15)
+    assert np.allclose(cw, [10.0 - 2.0, 20.0 + 1.0, 30.0 + 3.0], atol=1e-12)
+    nw, _ = orc.to_world([0.0, 1.0, 0.0], [0.0, 0.0, 0.0], P)
+    assert np.allclose(nw, [-1.0, 0.0, 0.0], atol=1e-15)
+    # pitch -90 deg about world x (rows of R: (1,0,0), (0,0,1), (0,-1,0)): a
+    # camera looking along its +z sees the floor normal (0,-1,0)... maps to +z up
+    Px = [1, 0, 0, 0.5, 0, 0, 1, 0.0, 0, -1, 0, 2.0, 0, 0, 0, 1]
+    nw, cw = orc.to_world([0.0, -1.0, 0.0], [0.0, 0.0, 1.5], Px)
+    assert np.allclose(nw, [0.0, 0.0, 1.0]) and np.allclose(cw, [0.5, 1.5, 2.0])
+    # the translation is the last column (indices 3, 7, 11), not the last row
+    nw, cw = orc.to_world([0.0, 0.0, 1.0], [0.0, 0.0, 0.0], [1, 0, 0, 4, 0, 1, 0, 5, 0, 0, 1, 6, 7, 8, 9, 1])
+    assert cw == [4.0, 5.0, 6.0] and nw == [0.0, 0.0, 1.0]
+
+
+def _oplane(n, c, inliers=100, status=0):
+    return {"n": list(map(float, n)), "c": list(map(float, c)), "inliers": inliers, "status": status}
+
+
+def test_oracle_map_scenarios_from_spec():
+    prm = {"drift_tol": 0.05, "normal_tol": math.radians(10), "xy_radius": 0.5, "sigma_p": 1.0, "sigma_m": 1e-6}
+    floor = _oplane([0, 0, 1], [0.2, 0.1, 0.0], inliers=1000)
+    # empty map + one plane -> one entry, no drift update
+    m, x, P, match, zk = orc.merge_frame([], [floor], IDENT, 0.0, 1.0, prm)
+    assert match == [-1] and zk is None and len(m) == 1 and (x, P) == (0.0, 1.0)
+    assert m[0]["c"] == [0.2, 0.1, 0.0] and m[0]["w"] == 1000.0 and m[0]["n_obs"] == 1
+    # the same plane re-observed with +2 cm vertical odometry error,
+    # sigma_p >> sigma_m -> merged, z_k = 0.02, x -> 0.02, the stored height
+    # stays within 1 mm of the original
+    m2, x2, P2, match, zk = orc.merge_frame(m, [floor], _pose(t=(0, 0, 0.02)), x, P, prm)
+    assert match == [0] and abs(zk - 0.02) < 1e-12 and abs(x2 - 0.02) < 1e-5
+    assert len(m2) == 1 and abs(m2[0]["c"][2]) < 1e-3 and m2[0]["n_obs"] == 2 and m2[0]["w"] == 2000.0
+    # dz = 8 cm > 5 cm -> inserted as a separate entry, no drift update
+    m3, x3, _, match, zk = orc.merge_frame(m, [floor], _pose(t=(0, 0, 0.08)), 0.0, 1.0, prm)
+    assert match == [-1] and zk is None and len(m3) == 2 and x3 == 0.0
+    assert abs(m3[1]["c"][2] - 0.08) < 1e-12
+    # 49 mm merges, 51 mm inserts (Eq. 5 with the 5 cm tolerance)
+    for dz, merged in [(0.049, True), (0.051, False)]:
+        _, _, _, match, _ = orc.merge_frame(m, [floor], _pose(t=(0, 0, dz)), 0.0, 1.0, prm)
+        assert (match == [0]) is merged
+    # rejected planes (status != OK) never enter the map
+    m4, _, _, match, _ = orc.merge_frame([], [_oplane([0, 0, 1], [0, 0, 0], status=1)], IDENT, 0.0, 1.0, prm)
+    assert match == [-1] and m4 == []
+    # the gate is on normals: a wall at the same height is not merged into the floor
+    wall = _oplane([1, 0, 0], [0.2, 0.1, 0.0])
+    m5, _, _, match, _ = orc.merge_frame(m, [wall], IDENT, 0.0, 1.0, prm)
+    assert match == [-1] and len(m5) == 2
+
+
+def _stair_world(steps=5):
+    return [([0.0, 0.0, 1.0], [0.3 * k + 0.15, 0.0, -0.15 * k]) for k in range(steps)]
+
+
+def _observe(treads, yaw, t_true):
+    """Camera-frame planes of world treads seen from the true pose (R, t_true)."""
+    R = np.array(_pose(yaw, t_true)).reshape(4, 4)[:3, :3]
+    t = np.array(t_true, float)
+    return [_oplane(R.T @ np.array(n), R.T @ (np.array(c) - t), inliers=2000) for n, c in treads]
+
+
+def _drift_run(compensate):
+    # SPEC acceptance 5 (S:676): linear vertical drift of 2 mm per frame over
+    # 50 frames; the odometry pose is the true pose shifted up by the drift
+    treads = _stair_world()
+    prm = {"drift_tol": 0.05, "normal_tol": math.radians(10), "xy_radius": 0.5,
+           "sigma_p": 1.0 if compensate else 0.0, "sigma_m": 1e-6 if compensate else 1e12}
+    m, x, P = [], 0.0, 1e-6
+    for k in range(50):
+        yaw = 0.2 * math.sin(0.3 * k)
+        t_true = (0.05 * k, 0.01 * k, 1.2)
+        drift = 0.002 * k
+        pose = _pose(yaw, (t_true[0], t_true[1], t_true[2] + drift))
+        m, x, P, _, _ = orc.merge_frame(m, _observe(treads, yaw, t_true), pose, x, P, prm)
+    err = max(min(abs(e["c"][2] - c[2]) for _, c in treads) for e in m)
+    return m, x, err
+
+
+def test_oracle_drift_tracking_acceptance():
+    m, x, err = _drift_run(True)
+    injected = 0.002 * 49
+    assert abs(x - injected) <= 0.2 * injected          # final x-hat within 20 % (S:676)
+    assert err <= 0.005                                 # every tread centroid within 5 mm of truth
+    assert len(m) == 5                                  # one entry per tread
+    # without compensation (filter frozen) the heights spread beyond 50 mm
+    m0, x0, err0 = _drift_run(False)
+    assert abs(x0) < 1e-9 and err0 > 0.05 and len(m0) > 5

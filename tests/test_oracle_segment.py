@@ -97,3 +97,34 @@ def test_stair_treads_become_regions():
     assert nr >= 4
     for r in range(nr):
         assert len(np.unique(face[lab == r])) == 1
+
+
+def test_normals_to_u8_fixed_values_channel_order_and_ties():
+    """Pins orc_normals_to_u8 (NEXT-2 input) to SPEC S:197's formula
+    round((n + 1) / 2 * 255) by hand-computed values, not a restatement.
+    Reading (Q26): `round` is round-half-to-even (Python 3's
+    round, C's rint); in f32, (n+1)/2*255 and (n+1)*127.5 are the same
+    single rounding of the same real number."""
+    H, W = 1, 5
+    n = np.zeros((3, H, W), np.float32)
+    n[0, 0] = [-1.0, -0.5, 0.0, 0.5, 1.0]          # x -> R
+    n[1, 0] = [1.0, 0.5, 0.0, -0.5, -1.0]          # y -> G
+    n[2, 0] = [0.0, 0.0, 0.0, 0.0, 0.0]            # z -> B: 127.5, a tie
+    u8 = oracle.normals_to_u8(n)
+    assert u8.shape == (H, W, 3)
+    # -1 -> 0; -0.5 -> 63.75 -> 64; 0 -> 127.5 -> 128 (tie to even); 0.5 -> 191.25 -> 191; 1 -> 255
+    assert u8[0, :, 0].tolist() == [0, 64, 128, 191, 255]
+    assert u8[0, :, 1].tolist() == [255, 191, 128, 64, 0]
+    assert u8[0, :, 2].tolist() == [128] * 5
+    # exact ties k + 1/2 (f32 inputs whose f32 product lands on the tie): k even
+    # rounds down, k odd rounds up (half-away-from-zero would give k + 1 for both)
+    for k in (100, 101):
+        target = np.float32(k + 0.5)
+        v = np.float32(k + 0.5) / np.float32(127.5) - np.float32(1)
+        cand = (np.arange(-4096, 4096, dtype=np.int64) + int(v.view(np.uint32))).astype(np.uint32).view(np.float32)
+        hit = cand[(cand + np.float32(1)) * np.float32(127.5) == target]
+        assert hit.size, f"no f32 input hits the tie {k}.5"
+        t = np.zeros((3, 1, hit.size), np.float32)
+        t[0, 0] = hit
+        got = oracle.normals_to_u8(t)[0, :, 0]
+        assert np.all(got == (k if k % 2 == 0 else k + 1)), (k, got)

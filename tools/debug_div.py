@@ -20,7 +20,7 @@ for sch in (pm.ADF_ALG1, pm.ADF_DIVERGENCE):
                                  normals=nrm)
             outs[(sch, T, nrm)] = o.cpu().numpy()
     o, _ = pm.adf_filter(d, fr["K"], fr["lam"], fr["kappa"], fr["iters"], iters_per_pass=4, scheme=sch,
-                         normals=False, engine=pm.ENGINE_STREAM)
+                         normals=False, engine=pm.ENGINE_REG)
     outs[(sch, "stream")] = o.cpu().numpy()
     ref = outs[(sch, "stream")]
     for k, v in outs.items():

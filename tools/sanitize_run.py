@@ -13,7 +13,7 @@ import scenegen
 
 fr = scenegen.make_config("C1n", holes=0.02)
 d, lab, K = fr["depth"].cuda(), fr["labels"].cuda(), fr["K"]
-for eng in (pm.ENGINE_TILED, pm.ENGINE_STREAM):
+for eng in (pm.ENGINE_TILED, pm.ENGINE_REG):
     for scheme in (pm.ADF_ALG1, pm.ADF_DIVERGENCE):
         out, nrm = pm.adf_filter(d, K, 0.15, 0.03, 10, engine=eng, scheme=scheme)
 pm.normals_from_depth(d, K)

@@ -17,7 +17,11 @@ out = torch.empty_like(depth)
 nrm = torch.empty(B, 3, bench.H, bench.W, device=dev)
 ws = torch.empty(pm.adf_workspace_bytes(bench.W, bench.H, B), dtype=torch.uint8, device=dev)
 ref = None
-for eng, T in [(1, 4), (1, 5), (2, 4), (2, 5), (2, 7), (2, 10), (2, 0)]:
+ENG = {1: "tiled", 3: "reg"}
+cfgs = [(1, 4), (1, 5), (3, 4), (3, 5)]
+if len(sys.argv) > 2:
+    cfgs = [tuple(map(int, c.split(":"))) for c in sys.argv[2].split(",")]
+for eng, T in cfgs:
     f = lambda: pm.adf_filter(depth, K, bench.LAM, bench.KAPPA, bench.ITERS, iters_per_pass=T, engine=eng, out=out,
                               normals_out=nrm, workspace=ws)
     for _ in range(3):
@@ -32,5 +36,5 @@ for eng, T in [(1, 4), (1, 5), (2, 4), (2, 5), (2, 7), (2, 10), (2, 0)]:
     if ref is None:
         ref = out.clone()
     same = torch.equal(out, ref)
-    print(f"engine={'tiled' if eng == 1 else 'stream'} T={T:2d} {ms:7.3f} ms/stage  {ms * 1e3 / B:6.2f} us/frame  "
+    print(f"engine={ENG[eng]:6s} T={T:2d} {ms:7.3f} ms/stage  {ms * 1e3 / B:6.2f} us/frame  "
           f"{bench.ITERS * bench.W * bench.H * B / ms / 1e9:6.2f} Gpix-iter/s  bitwise_same={same}")
