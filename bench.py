@@ -39,12 +39,16 @@ LAM, KAPPA, TAU, SEED = 0.15, 0.03, 0.01, 0x1919
 # algorithmic bytes of the fused ADF+normals stage per pixel: read depth 4 B,
 # write filtered depth 4 B, write normals 12 B
 ADF_ALG_BYTES_PX = 20
-# FP32 lane-ops of one Alg. 1 sweep at one pixel: 2gx, 2gy,
-# gy^2, gx^2+, exponent FFMA, ex2, three adds and an FFMA for the Laplacian,
-# the update FFMA
+# FP32 lane-ops of one Alg. 1 sweep at one pixel:
+# 2gx, 2gy, gy^2, gx^2+, exponent FFMA, ex2, three adds and an FFMA for the
+# Laplacian, the update FFMA
 ADF_OPS_PER_PIX_ITER = 11
-# one RANSAC point-hypothesis evaluation: 3 FFMA (n.p + d), compare, count
-RANSAC_OPS_PER_EVAL = 5
+# FP32 lane-ops of the Sobel + normal stage per pixel (~22 FP32 + 1 rsqrt)
+NORMAL_OPS_PER_PIX = 22
+# one RANSAC point-hypothesis evaluation: 3 FFMA (n.p + d), compare, count =
+# 5 issue slots; the issue bound is 148 SMs x 4 schedulers x
+# 32 lanes x clock / 5 evaluations per second
+RANSAC_ISSUE_PER_EVAL = 5
 WORKLOAD = ("C4 (BASELINE.json configs[3]): stream of distinct 640x480 D435-noise G-STAIR frames; ADF N=20 "
             "(lambda 0.15, kappa 0.03 m) + fused normals, RANSAC 64 regions x 64 hypotheses (tau 0.01 m) on the "
             "filtered depth")
@@ -78,6 +82,14 @@ class ClockSampler:
                0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
 
     def __init__(self, index: int, period_s: float = 0.002):
+        # NVML enumerates physical GPUs; honour CUDA_VISIBLE_DEVICES when it is a list of indices
+        vis = os.environ.get("CUDA_VISIBLE_DEVICES", "")
+        try:
+            ids = [int(x) for x in vis.split(",") if x.strip() != ""]
+            if ids and index < len(ids):
+                index = ids[index]
+        except ValueError:
+            pass
         self.index, self.period = index, period_s
         self.samples, self.reasons = [], set()
         self._stop = threading.Event()
@@ -218,6 +230,190 @@ def run_reference(args, rank, world):
 
 
 # --------------------------------------------------------------------------- CUDA arm
+def _events(n):
+    import torch
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(n)]
+    for e in ev:          # materialise the CUDA events (created lazily on first record)
+        e.record()
+    return ev
+
+
+def _alu_peak(clk_mhz):
+    """FP32 lane-op peak: 148 SMs x 128 lanes x SM clock (B200_PROFILING.md unit counts)."""
+    return 148 * 128 * clk_mhz * 1e6
+
+
+def _score_issue_peak(clk_mhz):
+    """RANSAC scoring issue bound: 148 SMs x 4 schedulers x 32
+    lanes x clock / 5 issue slots per point-hypothesis evaluation."""
+    return 148 * 4 * 32 * clk_mhz * 1e6 / RANSAC_ISSUE_PER_EVAL
+
+
+def stage_times(pm, depth, labels, K, iters, R, H_, first, ws, depth_out, normals, planes, lam=LAM, reps=5):
+    """Median per-stage device times (ms) of one batch, in the bench's launch
+    configuration on the launch stream: the ADF+normals stage (adf_filter),
+    and inside ransac_planes the compaction, hypotheses, scoring (the
+    dominant RANSAC kernel, its own events), selection + refit, plane table."""
+    import torch
+    out = {"adf_normals": [], "ransac": [], "compaction": [], "hypotheses": [], "score": [], "refit": []}
+    e0, e1 = _events(2)
+    ev = _events(pm.RANSAC_STAGE_EVENTS)
+    for _ in range(reps):
+        e0.record()
+        pm.adf_filter(depth, K, lam, KAPPA, iters, normals=True, out=depth_out, normals_out=normals, workspace=ws)
+        e1.record()
+        pm.ransac_planes(depth_out, K, labels, R, H_, TAU, SEED, first_frame_id=first, out=planes, workspace=ws,
+                         stage_events=ev)
+        torch.cuda.synchronize()
+        out["adf_normals"].append(e0.elapsed_time(e1))
+        out["ransac"].append(ev[0].elapsed_time(ev[5]))
+        out["compaction"].append(ev[0].elapsed_time(ev[1]))
+        out["hypotheses"].append(ev[1].elapsed_time(ev[2]))
+        out["score"].append(ev[2].elapsed_time(ev[3]))
+        out["refit"].append(ev[3].elapsed_time(ev[4]))
+    return {k: statistics.median(v) for k, v in out.items()}
+
+
+def rooflines(W_, H_, B, iters, n_hyp, labelled_px, st, clk_mhz, hbm_peak, traffic=None):
+    """ADF+normals stage: FP32 lane-ops (11 per pixel-iteration
+    + 22 per pixel for the normals) / stage time vs the FP32 peak, and its HBM
+    view (20 B/px algorithmic); RANSAC scoring: evaluations / score-kernel
+    time vs the §8(d) issue bound."""
+    px = W_ * H_ * B
+    adf_t = st["adf_normals"] / 1e3
+    ops = (iters * ADF_OPS_PER_PIX_ITER + NORMAL_OPS_PER_PIX) * px
+    alu = ops / adf_t
+    hbm = ADF_ALG_BYTES_PX * px / adf_t / 1e9
+    evals = n_hyp * labelled_px
+    ev_s = evals / (st["score"] / 1e3)
+    return ({"bound": "alu", "kernel": "adf_pass_kernel (ADF+normals stage, last pass fused with the normals)",
+             "achieved": alu / 1e12, "peak": _alu_peak(clk_mhz) / 1e12, "unit": "T FP32 lane-op/s",
+             "frac": alu / _alu_peak(clk_mhz), "traffic": traffic,
+             "alg_ops_per_pixel": iters * ADF_OPS_PER_PIX_ITER + NORMAL_OPS_PER_PIX,
+             "peak_source": "148 SMs x 128 FP32 lanes x SM clock (B200_PROFILING.md)",
+             "stage_ms": st["adf_normals"],
+             "hbm": {"achieved": hbm, "peak": hbm_peak, "unit": "GB/s", "frac": hbm / hbm_peak,
+                     "alg_bytes_per_px": ADF_ALG_BYTES_PX}},
+            {"bound": "issue", "kernel": "ransac_score_kernel (Alg. 2 l.9-13), its own CUDA-event time",
+             "achieved": ev_s / 1e12, "peak": _score_issue_peak(clk_mhz) / 1e12, "unit": "T evals/s",
+             "frac": ev_s / _score_issue_peak(clk_mhz), "evals": evals, "score_ms": st["score"],
+             "issue_slots_per_eval": RANSAC_ISSUE_PER_EVAL,
+             "stage_ms": {k: st[k] for k in ("ransac", "compaction", "hypotheses", "score", "refit")}})
+
+
+def _labelled(depth, labels, R):
+    import torch
+    v = (depth > 0) & torch.isfinite(depth) & (labels >= 0) & (labels < R)
+    return int(v.sum().item())
+
+
+def _time_pipeline(pm, depth, labels, K, iters, R, H_, first, steps, warmup, bufs):
+    import torch
+    d_out, nrm, planes, ws = bufs
+    f = lambda: pm.process_frames(depth, labels, K, LAM, KAPPA, iters, R, H_, TAU, SEED, first_frame_id=first,
+                                  depth_out=d_out, normals_out=nrm, planes_out=planes, workspace=ws)
+    for _ in range(warmup):
+        f()
+    torch.cuda.synchronize()
+    e0, e1 = _events(2)
+    e0.record()
+    for _ in range(steps):
+        f()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / steps
+
+
+def extra_configs(pm, dev, clk_mhz, hbm_peak):
+    """The other BASELINE.json configs and the paper's per-frame context, on
+    this GPU (bounded: ~1-2 s each).  Every number is device time with CUDA
+    events on the launch stream, inputs resident in HBM."""
+    import torch
+    import scenegen
+    res = {}
+
+    def bufs(B, H, W, R, H_):
+        return (torch.empty(B, H, W, device=dev), torch.empty(B, 3, H, W, device=dev),
+                torch.empty(B, R, pm.PLANE_WORDS, dtype=torch.int32, device=dev),
+                torch.empty(pm.pipeline_workspace_bytes(W, H, R, H_, B), dtype=torch.uint8, device=dev))
+
+    # C4 with 1 % dropout holes (SPEC S:510, S:673): every tile takes the hole-aware path
+    B = 512
+    d, lab, K = scenegen.stair_stream(0, B, W, H, REGIONS, device=dev)
+    for i in range(B):
+        d[i] = scenegen.dropout(d[i], 0.01, 1000 + i, i)
+    bb = bufs(B, H, W, REGIONS, HYPS)
+    ms = _time_pipeline(pm, d, lab, K, ITERS, REGIONS, HYPS, 0, 5, 2, bb)
+    st = stage_times(pm, d, lab, K, ITERS, REGIONS, HYPS, 0, bb[3], bb[0], bb[1], bb[2], reps=3)
+    res["C4_holes_1pct"] = {"value": B / (ms / 1e3), "unit": "frames/s", "frames_per_step": B, "ms_per_step": ms,
+                            "stages_ms": st, "workload": "C4 stream with 1 % hash-selected dropout holes per frame"}
+    del d, lab, bb
+    torch.cuda.empty_cache()
+
+    # C2: one 640x480 frame, N=20, R=32, H=64 -- per-frame latency, eager launches and a CUDA graph
+    fr = scenegen.make_config("C2", device=dev)
+    d1 = fr["depth"].to(dev)[None].contiguous()
+    l1 = fr["labels"].to(dev)[None].contiguous()
+    bb = bufs(1, fr["H"], fr["W"], fr["n_regions"], fr["n_hyp"])
+    call = lambda: pm.process_frames(d1, l1, fr["K"], LAM, KAPPA, fr["iters"], fr["n_regions"], fr["n_hyp"], TAU,
+                                     SEED, depth_out=bb[0], normals_out=bb[1], planes_out=bb[2], workspace=bb[3])
+    eager = _time_pipeline(pm, d1, l1, fr["K"], fr["iters"], fr["n_regions"], fr["n_hyp"], 0, 200, 20, bb)
+    s = torch.cuda.Stream(device=dev)
+    s.wait_stream(torch.cuda.current_stream(dev))
+    with torch.cuda.stream(s):
+        for _ in range(3):
+            call()
+    torch.cuda.current_stream(dev).wait_stream(s)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        call()
+    ref = bb[2].clone()
+    for _ in range(20):
+        g.replay()
+    torch.cuda.synchronize()
+    e0, e1 = _events(2)
+    n = 300
+    e0.record()
+    for _ in range(n):
+        g.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    graph_ms = e0.elapsed_time(e1) / n
+    same = bool(torch.equal(bb[2], ref))
+    res["C2_single_frame"] = {
+        "latency_ms_eager": eager, "latency_ms_graph": graph_ms, "hz_graph": 1e3 / graph_ms,
+        "graph_replay_bitwise_equal": same, "kernels_per_frame": pm.pipeline_kernel_launches(fr["iters"],
+                                                                                           fr["n_regions"]),
+        "workload": "BASELINE.json configs[1]: one 640x480 D435-noise G-STAIR frame, N=20, R=32, H=64",
+        "paper_context": "'>30 Hz' (P:10), 7.5 ms per frame (P:501), 'below 15 ms' (P:539) on the paper's own "
+                         "hardware (RTX 4060 laptop class, P:430) -- context, not a target"}
+    del d1, l1, bb, g
+    torch.cuda.empty_cache()
+
+    # C3 (1280x720 spiral, N=50, R=128 x 256 hypotheses) and C5 (4096x3072 terrain, N=100, R=1024)
+    for name, B in (("C3", 32), ("C5", 4)):
+        frs = [scenegen.make_config(name, frame=i, device=dev) for i in range(B)]
+        fr = frs[0]
+        d = torch.stack([f["depth"].to(dev) for f in frs]).contiguous()
+        lab = torch.stack([f["labels"].to(dev) for f in frs]).contiguous()
+        del frs
+        bb = bufs(B, fr["H"], fr["W"], fr["n_regions"], fr["n_hyp"])
+        ms = _time_pipeline(pm, d, lab, fr["K"], fr["iters"], fr["n_regions"], fr["n_hyp"], 0, 3, 1, bb)
+        st = stage_times(pm, d, lab, fr["K"], fr["iters"], fr["n_regions"], fr["n_hyp"], 0, bb[3], bb[0], bb[1],
+                         bb[2], reps=3)
+        rf, rr = rooflines(fr["W"], fr["H"], B, fr["iters"], fr["n_hyp"], _labelled(bb[0], lab, fr["n_regions"]),
+                           st, clk_mhz, hbm_peak)
+        res[name] = {"value": B / (ms / 1e3), "unit": "frames/s", "frames_per_step": B, "ms_per_step": ms,
+                     "adf_alu_frac": rf["frac"], "adf_hbm_frac": rf["hbm"]["frac"], "score_issue_frac": rr["frac"],
+                     "stages_ms": st,
+                     "workload": f"BASELINE.json {name}: {fr['W']}x{fr['H']}, N={fr['iters']}, "
+                                 f"R={fr['n_regions']}, H={fr['n_hyp']}"}
+        del d, lab, bb
+        torch.cuda.empty_cache()
+    return res
+
+
 def run_cuda(args, rank, world, local_rank):
     import torch
     import torch.distributed as dist
@@ -270,33 +466,16 @@ def run_cuda(args, rank, world, local_rank):
     ms_max = float(t.item())
     value = world * B * args.steps / (ms_max / 1e3)
 
-    # ---- per-stage times (same launch configuration, same stream), for the roofline
-    adf_ms, rs_ms = [], []
-    for _ in range(max(3, min(args.steps, 10))):
-        e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
-        e[0].record(stream)
-        pm.adf_filter(depth, K, LAM, KAPPA, ITERS, normals=True, out=depth_out, normals_out=normals, workspace=ws)
-        e[1].record(stream)
-        pm.ransac_planes(depth_out, K, labels, REGIONS, HYPS, TAU, SEED, first_frame_id=first, out=planes,
-                         workspace=ws)
-        e[2].record(stream)
-        torch.cuda.synchronize(dev)
-        adf_ms.append(e[0].elapsed_time(e[1]))
-        rs_ms.append(e[1].elapsed_time(e[2]))
-    adf_t = statistics.median(adf_ms) / 1e3
-    rs_t = statistics.median(rs_ms) / 1e3
+    # ---- per-stage / per-kernel times (same launch configuration, same stream), for the rooflines
+    st = stage_times(pm, depth, labels, K, ITERS, REGIONS, HYPS, first, ws, depth_out, normals, planes,
+                     reps=max(3, min(args.steps, 10)))
     peak, peak_src = _peaks()
-    adf_bytes = ADF_ALG_BYTES_PX * W * H * B
-    achieved_hbm = adf_bytes / adf_t / 1e9
-    n_pass = pm.pipeline_kernel_launches(ITERS, 0)
-    # ALU view of the same stage: Alg. 1 ℓ4-6 costs ADF_OPS_PER_PIX_ITER
-    # FP32 lane-operations per pixel-iteration; the stage's binding roofline is
-    # the SM issue/FP32 rate 148 SMs x 128 lanes x the SM clock.
-    pix_iter_per_s = ITERS * W * H * B / adf_t
-    alu_peak = 148 * 128 * (clocks.max_mhz or 1965) * 1e6 / 1e12          # T lane-ops/s
-    alu_achieved = pix_iter_per_s * ADF_OPS_PER_PIX_ITER / 1e12
-    rs_evals_per_s = HYPS * W * H * B / rs_t
-    traffic = _ncu_traffic()
+    clk = clocks.summary().get("sm_mhz") or clocks.max_mhz or 1965
+    roof, rs_roof = rooflines(W, H, B, ITERS, HYPS, _labelled(depth_out, labels, REGIONS), st, clk, peak,
+                              _ncu_traffic())
+    roof["hbm"]["peak_source"] = peak_src
+    roof["clock_mhz"] = clk
+    rs_roof["clock_mhz"] = clk
     # ---- e2e: host-resident inputs through the public C-ABI host entry
     # (pm_process_frames_host): pinned sensor-native uint16 depth (mm) and
     # uint8 labels (64 regions) in, plane table out; H2D of every input byte and D2H of
@@ -333,9 +512,16 @@ def run_cuda(args, rank, world, local_rank):
     e2e_value = world * B * args.steps / (float(te.item()) / 1e3)
     e2e_h2d = B * W * H * (2 + 1)
     e2e_d2h = B * REGIONS * 48
+    del arena
+    torch.cuda.empty_cache()
 
     # ---- final gather of the plane tables (the only collective)
     gather_tables(planes, world, rank)
+
+    # ---- the other configs and the per-frame context (rank 0, N = 1)
+    extra = None
+    if rank == 0 and world == 1 and not args.no_extra:
+        extra = extra_configs(pm, dev, clk, peak)
 
     # ---- oracle baseline on the host cores (rank 0, N = 1 only)
     cpu = None
@@ -343,7 +529,6 @@ def run_cuda(args, rank, world, local_rank):
         import oracle
         oracle.build()
         cores = _cpu_cores()
-        n1, _ = 1, None
         frames = [(depth[0].cpu().numpy(), labels[0].cpu().numpy())]
         _, t1 = _oracle_throughput(frames, K, first, 1)
         n = int(min(max(cores, round(args.cpu_seconds / max(t1, 1e-3))), 8 * cores, B))
@@ -363,22 +548,10 @@ def run_cuda(args, rank, world, local_rank):
                        "frames_per_rank": B, "global_frames_per_step": world * B,
                        "l2": f"inputs larger than L2 ({B * W * H * 8 / 2**20:.0f} MiB depth+labels per rank)",
                        "parallelism": f"frame-sharded x{world}"},
-            "roofline": {"bound": "alu", "kernel": f"adf_pass_kernel (ADF+normals stage: {n_pass} launches, "
-                                                   "last fused with the normals)",
-                         "achieved": alu_achieved, "peak": alu_peak, "unit": "T FP32 lane-op/s",
-                         "frac": alu_achieved / alu_peak, "traffic": traffic,
-                         "peak_source": "148 SMs x 128 FP32 lanes x max SM clock (B200_PROFILING.md)",
-                         "alg_ops_per_pixel_iter": ADF_OPS_PER_PIX_ITER, "pixel_iters_per_s": pix_iter_per_s,
-                         "hbm": {"achieved": achieved_hbm, "peak": peak, "unit": "GB/s",
-                                 "frac": achieved_hbm / peak, "alg_bytes_per_stage": adf_bytes,
-                                 "peak_source": peak_src}},
-            "ransac_roofline": {"bound": "alu", "kernel": "ransac_score_kernel (Alg. 2 l.9-13)",
-                                "achieved": rs_evals_per_s * RANSAC_OPS_PER_EVAL / 1e12, "peak": alu_peak,
-                                "unit": "T FP32 lane-op/s",
-                                "frac": rs_evals_per_s * RANSAC_OPS_PER_EVAL / 1e12 / alu_peak,
-                                "evals_per_s": rs_evals_per_s, "alg_ops_per_eval": RANSAC_OPS_PER_EVAL,
-                                "stage_ms_incl_compaction_refit": rs_t * 1e3},
-            "stages_ms": {"adf_normals": adf_t * 1e3, "ransac_incl_compaction": rs_t * 1e3},
+            "roofline": roof,
+            "ransac_roofline": rs_roof,
+            "stages_ms": st,
+            "configs": extra,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "frames/s", "h2d_bytes_per_step": e2e_h2d,
                     "d2h_bytes_per_step": e2e_d2h, "api": "pm_process_frames_host (uint16 mm depth + uint8 labels, "
@@ -392,6 +565,31 @@ def run_cuda(args, rank, world, local_rank):
     return 0
 
 
+def _free_port():
+    import socket
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
+def _self_launch(n):
+    """`bench.py --gpus N` outside torchrun: start N ranks (one per GPU, NCCL)
+    through torch.distributed.run on this node, exactly as the driver does."""
+    import torch
+    have = torch.cuda.device_count()
+    if have < n:
+        print(json.dumps({"error": f"--gpus {n} needs {n} visible GPUs, found {have}"}), flush=True)
+        return 2
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")            # NCCL's communicator log (nranks) on stderr
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    env.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    import subprocess
+    return subprocess.call(cmd, env=env)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -401,6 +599,7 @@ def main():
     ap.add_argument("--frames-per-rank", type=int, default=512)
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="CPU work budget of the oracle baseline")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extra", action="store_true", help="skip the C2/C3/C5/holes extra configs")
     ap.add_argument("--e2e-chunk", type=int, default=64, help="frames per chunk of the host pipeline")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))
@@ -408,7 +607,12 @@ def main():
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
         return run_reference(args, rank, world)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return _self_launch(args.gpus)
     if world > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)

@@ -198,7 +198,13 @@ typedef struct {
                                  -1 = invalid hypothesis                                */
     uint64_t* errq_out;       /* nullable device [B][n_regions][n_hyp]: Σ rint(min(d,64)
                                  * 2^24) per h (required work for PM_SELECT_ERROR)     */
+    void* const* stage_events;/* nullable host array of PM_RANSAC_STAGE_EVENTS
+                                 cudaEvent_t (created by the caller): recorded on the
+                                 stream before compaction and after compaction,
+                                 hypotheses, scoring, selection + refit and the plane
+                                 table -- per-kernel timing with CUDA events (bench) */
 } pm_ransac_options;
+enum { PM_RANSAC_STAGE_EVENTS = 6 };
 PM_API pm_status pm_ransac_planes_ex(const float* depth, int32_t W, int32_t H, int32_t n_frames,
                                      uint32_t first_frame_id, const pm_intrinsics* K,
                                      const int32_t* region_labels, int32_t n_regions,

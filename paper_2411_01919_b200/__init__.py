@@ -55,7 +55,11 @@ class pm_segment_params(ctypes.Structure):
 
 class pm_ransac_options(ctypes.Structure):
     _fields_ = [("sampler", ctypes.c_int32), ("select", ctypes.c_int32),
-                ("counts_out", ctypes.c_void_p), ("errq_out", ctypes.c_void_p)]
+                ("counts_out", ctypes.c_void_p), ("errq_out", ctypes.c_void_p),
+                ("stage_events", ctypes.c_void_p)]
+
+
+RANSAC_STAGE_EVENTS = 6
 
 
 _P, _I32, _U32, _U64, _F32, _SZ = (ctypes.c_void_p, ctypes.c_int32, ctypes.c_uint32, ctypes.c_uint64,
@@ -153,6 +157,34 @@ def _workspace(nbytes: int, device) -> torch.Tensor:
     return torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=device)
 
 
+def _out(t, shape, dtype, device, name: str) -> torch.Tensor:
+    """Allocate an output, or check a caller's: same device, dtype, contiguous,
+    exactly the element count the call writes (the library trusts pointers)."""
+    if t is None:
+        return torch.empty(shape, dtype=dtype, device=device)
+    n = 1
+    for d in shape:
+        n *= int(d)
+    if t.device != device or t.dtype != dtype or not t.is_contiguous() or t.numel() != n:
+        raise PMError(f"pmap: {name} must be a contiguous {dtype} tensor of {n} elements on {device}")
+    return t
+
+
+def _ws(t, nbytes: int, device, name: str = "workspace") -> torch.Tensor:
+    """A caller's workspace must be contiguous uint8 memory on the call's
+    device (the library checks its size and alignment)."""
+    if t is None:
+        return _workspace(nbytes, device)
+    if t.device != device or t.dtype != torch.uint8 or not t.is_contiguous():
+        raise PMError(f"pmap: {name} must be a contiguous uint8 tensor on {device}")
+    return t
+
+
+def _same_shape(a: torch.Tensor, b: torch.Tensor, what: str) -> None:
+    if tuple(a.shape) != tuple(b.shape) or a.device != b.device:
+        raise PMError(f"pmap: {what} must have the depth's shape and device")
+
+
 def pipeline_kernel_launches(iters: int, n_regions: int) -> int:
     return int(_lib.pm_pipeline_kernel_launches(int(iters), int(n_regions)))
 
@@ -176,16 +208,18 @@ def adf_filter(depth: torch.Tensor, K, lam: float, kappa: float, iters: int, nor
     """Alg. 1 on [H, W] or [B, H, W] f32 depth (metres, CUDA).
     Returns (I_smooth, normals [.., 3, H, W] or None)."""
     B, H, W = _frames(depth, torch.float32)
-    out = torch.empty_like(depth) if out is None else out
+    dev = depth.device
+    out = _out(out, depth.shape, torch.float32, dev, "out")
     nrm = None
     if normals:
         shape = (3, H, W) if depth.dim() == 2 else (B, 3, H, W)
-        nrm = torch.empty(shape, dtype=torch.float32, device=depth.device) if normals_out is None else normals_out
-    ws = workspace if workspace is not None else _workspace(adf_workspace_bytes(W, H, B), depth.device)
+        nrm = _out(normals_out, shape, torch.float32, dev, "normals_out")
+    ws = _ws(workspace, adf_workspace_bytes(W, H, B), dev)
     opt = pm_adf_options(int(iters_per_pass), int(scheme), int(normals_mode), int(engine))
-    _check(_lib.pm_adf_filter_ex(depth.data_ptr(), out.data_ptr(), W, H, B, ctypes.byref(_K(K)), float(lam),
-                                 float(kappa), int(iters), nrm.data_ptr() if nrm is not None else None,
-                                 ws.data_ptr(), ws.numel(), ctypes.byref(opt), _stream(depth)))
+    with torch.cuda.device(dev):
+        _check(_lib.pm_adf_filter_ex(depth.data_ptr(), out.data_ptr(), W, H, B, ctypes.byref(_K(K)), float(lam),
+                                     float(kappa), int(iters), nrm.data_ptr() if nrm is not None else None,
+                                     ws.data_ptr(), ws.numel(), ctypes.byref(opt), _stream(depth)))
     return out, nrm
 
 
@@ -193,9 +227,10 @@ def normals_from_depth(depth: torch.Tensor, K, out: torch.Tensor = None, mode: i
     """Alg. 1 ℓ9-13 on [H, W] or [B, H, W] f32 depth -> [.., 3, H, W]."""
     B, H, W = _frames(depth, torch.float32)
     shape = (3, H, W) if depth.dim() == 2 else (B, 3, H, W)
-    out = torch.empty(shape, dtype=torch.float32, device=depth.device) if out is None else out
-    _check(_lib.pm_normals_from_depth_ex(depth.data_ptr(), W, H, B, ctypes.byref(_K(K)), int(mode), out.data_ptr(),
-                                         _stream(depth)))
+    out = _out(out, shape, torch.float32, depth.device, "out")
+    with torch.cuda.device(depth.device):
+        _check(_lib.pm_normals_from_depth_ex(depth.data_ptr(), W, H, B, ctypes.byref(_K(K)), int(mode),
+                                             out.data_ptr(), _stream(depth)))
     return out
 
 
@@ -239,30 +274,35 @@ class Planes(NamedTuple):
 def ransac_planes(depth: torch.Tensor, K, labels: torch.Tensor, n_regions: int, n_hyp: int, tau: float,
                   seed: int, first_frame_id: int = 0, sampler: int = SAMPLER_PHILOX,
                   select: int = SELECT_COUNT, debug: bool = False, out: torch.Tensor = None,
-                  workspace: torch.Tensor = None):
+                  workspace: torch.Tensor = None, stage_events=None):
     """Alg. 2 over every region of every frame.  Returns Planes
     (and, with debug=True, per-hypothesis counts / errq tensors [.., R, n_hyp];
     debug="counts": counts only, errq None -- the scoring kernel without the
     error sums, i.e. the one the default call runs)."""
     B, H, W = _frames(depth, torch.float32)
-    if tuple(labels.shape) != tuple(depth.shape):
-        raise PMError("pmap: labels must have the depth's shape")
+    _same_shape(labels, depth, "labels")
     _frames(labels, torch.int32)
     lead = () if depth.dim() == 2 else (B,)
-    out = torch.empty(lead + (n_regions, PLANE_WORDS), dtype=torch.int32, device=depth.device) if out is None else out
-    ws = workspace if workspace is not None else _workspace(
-        ransac_workspace_bytes(W, H, n_regions, n_hyp, B), depth.device)
+    out = _out(out, lead + (n_regions, PLANE_WORDS), torch.int32, depth.device, "out")
+    ws = _ws(workspace, ransac_workspace_bytes(W, H, n_regions, n_hyp, B), depth.device)
     counts = errq = None
     if debug:
         counts = torch.empty(lead + (n_regions, n_hyp), dtype=torch.int32, device=depth.device)
     if debug and debug != "counts":   # "counts": counts only (keeps the default scoring kernel)
         errq = torch.empty(lead + (n_regions, n_hyp), dtype=torch.int64, device=depth.device)
+    ev_arr = None
+    if stage_events is not None:   # RANSAC_STAGE_EVENTS torch.cuda.Event objects (timing)
+        if len(stage_events) != RANSAC_STAGE_EVENTS:
+            raise PMError(f"pmap: stage_events needs {RANSAC_STAGE_EVENTS} events")
+        ev_arr = (ctypes.c_void_p * RANSAC_STAGE_EVENTS)(*[e.cuda_event for e in stage_events])
     opt = pm_ransac_options(int(sampler), int(select), counts.data_ptr() if counts is not None else None,
-                            errq.data_ptr() if errq is not None else None)
-    _check(_lib.pm_ransac_planes_ex(depth.data_ptr(), W, H, B, int(first_frame_id), ctypes.byref(_K(K)),
-                                    labels.data_ptr(), int(n_regions), int(n_hyp), float(tau),
-                                    int(seed) & (2**64 - 1), out.data_ptr(), ws.data_ptr(), ws.numel(),
-                                    ctypes.byref(opt), _stream(depth)))
+                            errq.data_ptr() if errq is not None else None,
+                            ctypes.cast(ev_arr, ctypes.c_void_p) if ev_arr is not None else None)
+    with torch.cuda.device(depth.device):
+        _check(_lib.pm_ransac_planes_ex(depth.data_ptr(), W, H, B, int(first_frame_id), ctypes.byref(_K(K)),
+                                        labels.data_ptr(), int(n_regions), int(n_hyp), float(tau),
+                                        int(seed) & (2**64 - 1), out.data_ptr(), ws.data_ptr(), ws.numel(),
+                                        ctypes.byref(opt), _stream(depth)))
     planes = Planes(out)
     return (planes, counts, errq) if debug else planes
 
@@ -274,19 +314,20 @@ def process_frames(depth: torch.Tensor, labels: torch.Tensor, K, lam: float, kap
     """The whole per-frame path in one C-ABI call (pm_process_frames):
     adf_filter with fused normals, then ransac_planes on the filtered depth."""
     B, H, W = _frames(depth, torch.float32)
+    _same_shape(labels, depth, "labels")
     _frames(labels, torch.int32)
     lead = () if depth.dim() == 2 else (B,)
     dev = depth.device
-    depth_out = torch.empty_like(depth) if depth_out is None else depth_out
-    normals_out = torch.empty(lead + (3, H, W), dtype=torch.float32, device=dev) if normals_out is None else normals_out
-    planes_out = torch.empty(lead + (n_regions, PLANE_WORDS), dtype=torch.int32, device=dev) if planes_out is None else planes_out
-    ws = workspace if workspace is not None else _workspace(
-        pipeline_workspace_bytes(W, H, n_regions, n_hyp, B), dev)
-    _check(_lib.pm_process_frames(depth.data_ptr(), labels.data_ptr(), W, H, B, int(first_frame_id),
-                                  ctypes.byref(_K(K)), float(lam), float(kappa), int(iters), int(n_regions),
-                                  int(n_hyp), float(tau), int(seed) & (2**64 - 1), depth_out.data_ptr(),
-                                  normals_out.data_ptr(), planes_out.data_ptr(), ws.data_ptr(), ws.numel(),
-                                  _stream(depth)))
+    depth_out = _out(depth_out, depth.shape, torch.float32, dev, "depth_out")
+    normals_out = _out(normals_out, lead + (3, H, W), torch.float32, dev, "normals_out")
+    planes_out = _out(planes_out, lead + (n_regions, PLANE_WORDS), torch.int32, dev, "planes_out")
+    ws = _ws(workspace, pipeline_workspace_bytes(W, H, n_regions, n_hyp, B), dev)
+    with torch.cuda.device(dev):
+        _check(_lib.pm_process_frames(depth.data_ptr(), labels.data_ptr(), W, H, B, int(first_frame_id),
+                                      ctypes.byref(_K(K)), float(lam), float(kappa), int(iters), int(n_regions),
+                                      int(n_hyp), float(tau), int(seed) & (2**64 - 1), depth_out.data_ptr(),
+                                      normals_out.data_ptr(), planes_out.data_ptr(), ws.data_ptr(), ws.numel(),
+                                      _stream(depth)))
     return depth_out, normals_out, Planes(planes_out)
 
 
@@ -299,9 +340,10 @@ def depth_u16_to_metres(depth_mm: torch.Tensor, out: torch.Tensor = None, scale:
     """uint16 millimetres -> f32 metres on the device (0 stays 0 = invalid)."""
     if depth_mm.dtype != torch.uint16 or not depth_mm.is_cuda or not depth_mm.is_contiguous():
         raise PMError("pmap: expected a contiguous CUDA uint16 tensor")
-    out = torch.empty(depth_mm.shape, dtype=torch.float32, device=depth_mm.device) if out is None else out
-    _check(_lib.pm_depth_u16_to_metres(depth_mm.data_ptr(), out.data_ptr(), depth_mm.numel(), float(scale),
-                                       _stream(out)))
+    out = _out(out, depth_mm.shape, torch.float32, depth_mm.device, "out")
+    with torch.cuda.device(depth_mm.device):
+        _check(_lib.pm_depth_u16_to_metres(depth_mm.data_ptr(), out.data_ptr(), depth_mm.numel(), float(scale),
+                                           _stream(out)))
     return out
 
 
@@ -323,10 +365,16 @@ def process_frames_host(depth: torch.Tensor, labels: torch.Tensor, K, lam: float
     B, H, W = depth.shape
     dev = torch.device("cuda") if device is None else torch.device(device)
     C = min(int(chunk_frames), B)
-    if arena is None:
-        arena = torch.empty(host_pipeline_arena_bytes(W, H, n_regions, n_hyp, C, dfmt, lfmt), dtype=torch.uint8,
-                            device=dev)
-    planes_out = torch.empty(B, n_regions, PLANE_WORDS, dtype=torch.int32) if planes_out is None else planes_out
+    if dev.type == "cuda" and dev.index is None:
+        dev = torch.device("cuda", torch.cuda.current_device())
+    arena = _ws(arena, 0, dev, "arena") if arena is not None else torch.empty(
+        host_pipeline_arena_bytes(W, H, n_regions, n_hyp, C, dfmt, lfmt), dtype=torch.uint8, device=dev)
+    cpu = torch.device("cpu")
+    planes_out = _out(planes_out, (B, n_regions, PLANE_WORDS), torch.int32, cpu, "planes_out")
+    if depth_out is not None:
+        depth_out = _out(depth_out, (B, H, W), torch.float32, cpu, "depth_out")
+    if normals_out is not None:
+        normals_out = _out(normals_out, (B, 3, H, W), torch.float32, cpu, "normals_out")
     with torch.cuda.device(dev):
         stream = torch.cuda.current_stream(dev).cuda_stream
         _check(_lib.pm_process_frames_host(depth.data_ptr(), dfmt, labels.data_ptr(), lfmt, W, H, B,
@@ -359,10 +407,12 @@ def segment_regions(normals: torch.Tensor, canny_low: float = 30.0, canny_high: 
     labels = torch.empty(B, H, W, dtype=torch.int32, device=dev)
     nreg = torch.empty(B, dtype=torch.int32, device=dev)
     emask = torch.empty(B, H, W, dtype=torch.uint8, device=dev) if edges else None
-    ws = workspace if workspace is not None else _workspace(segment_workspace_bytes(W, H, B, min_area), dev)
+    ws = _ws(workspace, segment_workspace_bytes(W, H, B, min_area), dev)
     prm = pm_segment_params(float(canny_low), float(canny_high), int(min_area), int(max_regions))
-    _check(_lib.pm_segment_regions(n4.data_ptr(), W, H, B, ctypes.byref(prm), labels.data_ptr(), nreg.data_ptr(),
-                                   emask.data_ptr() if edges else None, ws.data_ptr(), ws.numel(), _stream(normals)))
+    with torch.cuda.device(dev):
+        _check(_lib.pm_segment_regions(n4.data_ptr(), W, H, B, ctypes.byref(prm), labels.data_ptr(),
+                                       nreg.data_ptr(), emask.data_ptr() if edges else None, ws.data_ptr(),
+                                       ws.numel(), _stream(normals)))
     if single:
         labels = labels[0]
         emask = emask[0] if edges else None
@@ -465,12 +515,14 @@ def region_polygons(labels: torch.Tensor, n_regions: int, eps: float = 3.0, max_
     verts = torch.zeros(lead + (n_regions, max_vertices, 2), dtype=torch.int32, device=dev)
     nv = torch.empty(lead + (n_regions,), dtype=torch.int32, device=dev)
     nb = int(_lib.pm_region_polygons_workspace_bytes(B, n_regions, max_contour))
-    ws = workspace if workspace is not None else _workspace(nb, dev)
+    ws = _ws(workspace, nb, dev)
     prm = pm_polygon_params(int(round(eps * 16)), int(max_contour), int(max_vertices))
-    _check(_lib.pm_region_polygons(ctypes.c_void_p(labels.data_ptr()), W, H, B, int(n_regions), ctypes.byref(prm),
-                                   ctypes.c_void_p(clen.data_ptr()), ctypes.c_void_p(verts.data_ptr()),
-                                   ctypes.c_void_p(nv.data_ptr()), ctypes.c_void_p(ws.data_ptr()),
-                                   ctypes.c_size_t(ws.numel()), ctypes.c_void_p(_stream(labels))))
+    with torch.cuda.device(dev):
+        _check(_lib.pm_region_polygons(ctypes.c_void_p(labels.data_ptr()), W, H, B, int(n_regions),
+                                       ctypes.byref(prm), ctypes.c_void_p(clen.data_ptr()),
+                                       ctypes.c_void_p(verts.data_ptr()), ctypes.c_void_p(nv.data_ptr()),
+                                       ctypes.c_void_p(ws.data_ptr()), ctypes.c_size_t(ws.numel()),
+                                       ctypes.c_void_p(_stream(labels))))
     return Polygons(clen, verts, nv)
 
 
@@ -480,11 +532,12 @@ def rasterize_polygons(polys: Polygons, W: int, H: int, out: torch.Tensor = None
     single = nv.dim() == 1
     B = 1 if single else nv.shape[0]
     R, MV = v.shape[-3], v.shape[-2]
-    out = torch.empty(((H, W) if single else (B, H, W)), dtype=torch.int32, device=v.device) if out is None else out
+    out = _out(out, ((H, W) if single else (B, H, W)), torch.int32, v.device, "out")
     ws = _workspace(16 * B * max(R, 1), v.device)
-    _check(_lib.pm_rasterize_polygons(ctypes.c_void_p(v.data_ptr()), ctypes.c_void_p(nv.data_ptr()), MV, W, H, B, R,
-                                      ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(ws.data_ptr()),
-                                      ctypes.c_size_t(ws.numel()), ctypes.c_void_p(_stream(v))))
+    with torch.cuda.device(v.device):
+        _check(_lib.pm_rasterize_polygons(ctypes.c_void_p(v.data_ptr()), ctypes.c_void_p(nv.data_ptr()), MV, W, H,
+                                          B, R, ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(ws.data_ptr()),
+                                          ctypes.c_size_t(ws.numel()), ctypes.c_void_p(_stream(v))))
     return out
 
 
@@ -495,8 +548,12 @@ def lift_polygon_vertices(polys: Polygons, planes, K) -> torch.Tensor:
     B = 1 if single else nv.shape[0]
     R, MV = v.shape[-3], v.shape[-2]
     raw = planes.raw if hasattr(planes, "raw") else planes
+    if raw.device != v.device or raw.dtype != torch.int32 or not raw.is_contiguous() or \
+            raw.numel() != B * R * PLANE_WORDS:
+        raise PMError("pmap: planes must be the contiguous int32 plane table of the polygons' frames and regions")
     X = torch.empty(v.shape[:-1] + (3,), dtype=torch.float64, device=v.device)
-    _check(_lib.pm_lift_polygon_vertices(ctypes.c_void_p(v.data_ptr()), ctypes.c_void_p(nv.data_ptr()), MV,
-                                         ctypes.c_void_p(raw.data_ptr()), B, R, ctypes.byref(_K(K)),
-                                         ctypes.c_void_p(X.data_ptr()), ctypes.c_void_p(_stream(v))))
+    with torch.cuda.device(v.device):
+        _check(_lib.pm_lift_polygon_vertices(ctypes.c_void_p(v.data_ptr()), ctypes.c_void_p(nv.data_ptr()), MV,
+                                             ctypes.c_void_p(raw.data_ptr()), B, R, ctypes.byref(_K(K)),
+                                             ctypes.c_void_p(X.data_ptr()), ctypes.c_void_p(_stream(v))))
     return X

@@ -88,11 +88,13 @@ pm_status ransac_impl(const float* depth, int32_t W, int32_t H, int32_t B, uint3
     int sampler = PM_SAMPLER_PHILOX, select = PM_SELECT_COUNT;
     int32_t* counts_out = nullptr;
     uint64_t* errq_out = nullptr;
+    void* const* ev = nullptr;
     if (opt) {
         sampler = opt->sampler;
         select = opt->select;
         counts_out = opt->counts_out;
         errq_out = opt->errq_out;
+        ev = opt->stage_events;
         if (sampler != PM_SAMPLER_PHILOX && sampler != PM_SAMPLER_ENUMERATE) return PM_ERR_INVALID_ARGUMENT;
         if (select != PM_SELECT_COUNT && select != PM_SELECT_ERROR) return PM_ERR_INVALID_ARGUMENT;
     }
@@ -101,8 +103,10 @@ pm_status ransac_impl(const float* depth, int32_t W, int32_t H, int32_t B, uint3
     if (!ws || ws_bytes < need || !aligned256(ws)) return PM_ERR_WORKSPACE;
     if (cudaError_t e = setup(); e != cudaSuccess) return PM_ERR_CUDA;
     const pm::RansacWorkspace L = pm::ransac_workspace_layout(ws, W, H, R, n_hyp, B);
+    if (ev && cudaEventRecord((cudaEvent_t)ev[0], stream) != cudaSuccess) return PM_ERR_CUDA;
     cudaError_t e = pm::compact_run(depth, labels, L, stream, depth_all_valid);
     if (e != cudaSuccess) return PM_ERR_CUDA;
+    if (ev && cudaEventRecord((cudaEvent_t)ev[1], stream) != cudaSuccess) return PM_ERR_CUDA;
     pm::RansacArgs a;
     a.K = *K;
     a.tau = tau;
@@ -112,10 +116,21 @@ pm_status ransac_impl(const float* depth, int32_t W, int32_t H, int32_t B, uint3
     a.select = select;
     a.counts_out = counts_out;
     a.errq_out = errq_out;
+    a.stage_events = ev ? ev + 2 : nullptr;
     return cuda_status(pm::ransac_run(L, a, planes, stream));
 }
 
 }  // namespace
+
+namespace pm {
+pm_status pipeline_validate(int32_t W, int32_t H, int32_t B, const pm_intrinsics* K, float lam, float kappa,
+                            int32_t iters, int32_t R, int32_t n_hyp, float tau) {
+    if (!dims_ok(W, H, B) || !intrinsics_ok(K) || iters < 0) return PM_ERR_INVALID_ARGUMENT;
+    if (!(lam > 0.0f && lam <= 0.25f) || !finite_pos(kappa)) return PM_ERR_INVALID_ARGUMENT;
+    if (R < 0 || R > 65536 || n_hyp < 1 || n_hyp > 4096 || !finite_pos(tau)) return PM_ERR_INVALID_ARGUMENT;
+    return PM_OK;
+}
+}  // namespace pm
 
 extern "C" {
 

@@ -163,6 +163,10 @@ PM_API pm_status pm_process_frames_host(const void* depth_host, int32_t depth_fo
     if (!arena || arena_bytes < pm_host_pipeline_arena_bytes(W, H, n_regions, n_hyp, C, depth_format, label_format) ||
         ((uintptr_t)arena & 255u))
         return PM_ERR_WORKSPACE;
+    // every argument check before the first copy is queued
+    if (pm_status v = pipeline_validate(W, H, n_frames, K, lambda, kappa, iters, n_regions, n_hyp, inlier_thresh);
+        v != PM_OK)
+        return v;
     DeviceStreams* ds = streams_for_current_device();
     if (!ds || ds->err != cudaSuccess) return PM_ERR_CUDA;
     std::lock_guard<std::mutex> lk(ds->mu);
@@ -172,6 +176,16 @@ PM_API pm_status pm_process_frames_host(const void* depth_host, int32_t depth_fo
     const size_t dsz = depth_format == PM_DEPTH_U16_MM ? 2 : 4;
     const size_t lsz = label_format == PM_LABELS_U16 ? 2 : label_format == PM_LABELS_U8 ? 1 : 4;
     const int n_chunks = (n_frames + C - 1) / C;
+    // every exit waits for the copies already queued on the internal streams
+    // (and the kernels feeding them): the caller may free or reuse its host
+    // buffers and the arena as soon as this returns, also on error
+    auto finish = [&](pm_status st) {
+        const cudaError_t e1 = cudaStreamSynchronize(ds->copy);
+        const cudaError_t e2 = cudaStreamSynchronize(cs);
+        const cudaError_t e3 = cudaStreamSynchronize(ds->down);
+        if (st == PM_OK && (e1 != cudaSuccess || e2 != cudaSuccess || e3 != cudaSuccess)) st = PM_ERR_CUDA;
+        return st;
+    };
     cudaError_t e = cudaSuccess;
     // both slots start free
     for (int s = 0; s < 2 && e == cudaSuccess; ++s) e = cudaEventRecord(ds->freed[s], cs);
@@ -195,7 +209,7 @@ PM_API pm_status pm_process_frames_host(const void* depth_host, int32_t depth_fo
         if (e != cudaSuccess) break;
         if (depth_format == PM_DEPTH_U16_MM) {
             pm_status st = pm_depth_u16_to_metres((const uint16_t*)sl.raw_depth, sl.depth, px, 1e-3f, stream);
-            if (st != PM_OK) return st;
+            if (st != PM_OK) return finish(st);
         }
         if (label_format == PM_LABELS_U16) {
             u16_labels_kernel<<<(unsigned)((px + kConvThreads - 1) / kConvThreads), kConvThreads, 0, cs>>>(
@@ -209,7 +223,7 @@ PM_API pm_status pm_process_frames_host(const void* depth_host, int32_t depth_fo
         pm_status st = pm_process_frames(sl.depth, sl.labels, W, H, nf, first_frame_id + (uint32_t)f0, K, lambda,
                                          kappa, iters, n_regions, n_hyp, inlier_thresh, seed, sl.depth_out,
                                          sl.normals, sl.planes, sl.ws, sl.ws_bytes, stream);
-        if (st != PM_OK) return st;
+        if (st != PM_OK) return finish(st);
         e = cudaEventRecord(ds->done[s], cs);
         // D2H of the results on the download stream; the slot is free afterwards
         if (e == cudaSuccess) e = cudaStreamWaitEvent(ds->down, ds->done[s], 0);
@@ -224,10 +238,7 @@ PM_API pm_status pm_process_frames_host(const void* depth_host, int32_t depth_fo
                                 cudaMemcpyDeviceToHost, ds->down);
         if (e == cudaSuccess) e = cudaEventRecord(ds->freed[s], ds->down);
     }
-    if (e == cudaSuccess) e = cudaStreamSynchronize(ds->copy);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(ds->down);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(cs);
-    return e == cudaSuccess ? PM_OK : PM_ERR_CUDA;
+    return finish(e == cudaSuccess ? PM_OK : PM_ERR_CUDA);
 }
 
 }  // extern "C"

@@ -25,6 +25,10 @@ cudaError_t adf_reg_setup_attributes();
 cudaError_t normals_run(const float* depth, float* normals, int W, int H, int B,
                         const pm_intrinsics* K, int nmode, cudaStream_t stream);
 
+// ---- api.cu: the argument checks of pm_process_frames, without launching
+pm_status pipeline_validate(int32_t W, int32_t H, int32_t B, const pm_intrinsics* K, float lam, float kappa,
+                            int32_t iters, int32_t R, int32_t n_hyp, float tau);
+
 // ---- compact.cu / ransac.cu
 struct Sums;
 struct RansacWorkspace {
@@ -62,6 +66,7 @@ struct RansacArgs {
     int select;
     int32_t* counts_out;   // nullable debug
     uint64_t* errq_out;    // nullable debug
+    void* const* stage_events;   // nullable: 4 cudaEvent_t recorded after hyp, score, refit, finalize
 };
 cudaError_t ransac_setup_attributes();
 cudaError_t ransac_run(const RansacWorkspace& ws, const RansacArgs& a, pm_plane* planes,

@@ -733,7 +733,11 @@ cudaError_t ransac_run(const RansacWorkspace& ws, const RansacArgs& a, pm_plane*
     const bool need_err = a.select == PM_SELECT_ERROR || a.errq_out != nullptr;
     const int K = ws.score_K, L = ws.score_L;
     const int n_hyp_slots = ws.R * (ws.n_hyp_pad > K * L ? ws.n_hyp_pad : K * L);
+    auto mark = [&](int k) {
+        if (a.stage_events) cudaEventRecord((cudaEvent_t)a.stage_events[k], stream);
+    };
     ransac_hyp_kernel<<<dim3((n_hyp_slots + 255) / 256, ws.B), 256, 0, stream>>>(ws, a, need_err ? 1 : 0);
+    mark(0);
     const dim3 g_score((unsigned)(((size_t)ws.W * ws.H + kScoreChunk - 1) / kScoreChunk), ws.B);
     bool launched = false;
 #define PM_SCORE(KK, LL)                                                                                   \
@@ -750,11 +754,14 @@ cudaError_t ransac_run(const RansacWorkspace& ws, const RansacArgs& a, pm_plane*
     PM_SCORE(8, 64) PM_SCORE(8, 128) PM_SCORE(8, 256) PM_SCORE(16, 256)
 #undef PM_SCORE
     if (!launched) return cudaErrorInvalidConfiguration;
+    mark(1);
     const dim3 g_refit((unsigned)(((size_t)ws.W * ws.H + kRefitChunk - 1) / kRefitChunk), ws.B);
     ransac_select_kernel<<<dim3((ws.R + 7) / 8, ws.B), 256, 0, stream>>>(ws, a);
     ransac_refit_kernel<<<g_refit, kScoreThreads, kRefitSmem, stream>>>(ws, a);
+    mark(2);
     ransac_finalize_kernel<<<dim3((ws.R + kFinalThreads - 1) / kFinalThreads, ws.B), kFinalThreads, 0, stream>>>(
         ws, a, planes);
+    mark(3);
     return cudaGetLastError();
 }
 

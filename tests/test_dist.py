@@ -6,6 +6,7 @@ import socket
 import tempfile
 
 import numpy as np
+import pytest
 import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
@@ -56,3 +57,51 @@ def test_two_rank_sharding_matches_single_process():
     single = _tables(0, 2 * B_PER_RANK)
     assert torch.equal(gathered, single)
     assert bench.shard(1, 512) == (512, 512)
+
+
+# ------------------------------------------------------------------ CUDA path
+def _cuda_worker(rank, world, port, out_path, frames_per_rank):
+    """One rank of the frame-sharded CUDA path: its own shard of the C4-style
+    stream through pm.process_frames (no device-side collective: every rank's
+    kernels are independent), tables / depth / normals gathered over gloo."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import paper_2411_01919_b200 as pm
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    first, n = bench.shard(rank, frames_per_rank)
+    d, lab, K = scenegen.stair_stream(first, n, W, H, R, device=dev)
+    d_out, nrm, planes = pm.process_frames(d, lab, K, 0.15, 0.03, 20, R, HYP, 0.01, 0x1919, first_frame_id=first)
+    torch.cuda.synchronize()
+    parts = {}
+    for name, t in (("planes", planes.raw), ("depth", d_out), ("normals", nrm)):
+        parts[name] = bench.gather_tables(t.cpu(), world, rank)
+    if rank == 0:
+        torch.save(parts, out_path)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_two_rank_cuda_sharding_bitwise_equals_single_process():
+    """SURVEY §8(e) determinism on the CUDA path: two ranks (gloo, both on the
+    one GPU of this box; their kernels never wait on one another) each run
+    pm.process_frames on their shard; the gathered plane tables, filtered
+    depth and normals equal a single-process run over all frames bit for bit
+    (the RNG is keyed by the global frame id)."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2411_01919_b200 as pm
+    per_rank = 3
+    with tempfile.TemporaryDirectory() as td:
+        out = os.path.join(td, "gathered.pt")
+        mp.spawn(_cuda_worker, args=(2, _free_port(), out, per_rank), nprocs=2, join=True)
+        got = torch.load(out)
+    d, lab, K = scenegen.stair_stream(0, 2 * per_rank, W, H, R, device="cuda")
+    d_out, nrm, planes = pm.process_frames(d, lab, K, 0.15, 0.03, 20, R, HYP, 0.01, 0x1919)
+    torch.cuda.synchronize()
+    assert torch.equal(got["planes"], planes.raw.cpu())
+    assert torch.equal(got["depth"], d_out.cpu())
+    assert torch.equal(got["normals"], nrm.cpu())
+    assert (got["planes"][..., 10] == 0).any()       # some planes accepted: a non-trivial table

@@ -702,3 +702,51 @@ def test_reg_engine_batched_stream_equals_tiled(pm):
     ref, nref = pm.adf_filter(d, K, 0.15, 0.03, 20, engine=pm.ENGINE_TILED)
     out, nrm = pm.adf_filter(d, K, 0.15, 0.03, 20)
     assert torch.equal(out, ref) and torch.equal(nrm, nref)
+
+
+def test_binding_rejects_mismatched_buffers(pm):
+    """the binding checks every output / workspace tensor (device,
+    dtype, contiguity, element count) and the labels' shape before calling
+    the C ABI, which trusts its pointers."""
+    d, lab, K = scenegen.stair_stream(0, 2, 128, 96, 8, device=DEV)
+    bad = [dict(depth_out=torch.empty(2, 96, 127, device=DEV)),
+           dict(normals_out=torch.empty(2, 3, 96, 128, device=DEV, dtype=torch.float64)),
+           dict(planes_out=torch.empty(2, 8, 12, dtype=torch.int32)),                       # host memory
+           dict(planes_out=torch.empty(2, 12, 8, dtype=torch.int32, device=DEV).transpose(1, 2)),   # not contiguous
+           dict(workspace=torch.empty(10, dtype=torch.float32, device=DEV))]
+    for kw in bad:
+        with pytest.raises(pm.PMError):
+            pm.process_frames(d, lab, K, 0.15, 0.03, 4, 8, 16, 0.01, 1, **kw)
+    with pytest.raises(pm.PMError):              # [H, W] labels with [B, H, W] depth
+        pm.process_frames(d, lab[0].contiguous(), K, 0.15, 0.03, 4, 8, 16, 0.01, 1)
+    with pytest.raises(pm.PMError):
+        pm.ransac_planes(d, K, lab[:1].contiguous(), 8, 16, 0.01, 1)
+    with pytest.raises(pm.PMError):
+        pm.adf_filter(d, K, 0.15, 0.03, 4, out=torch.empty(3, 96, 128, device=DEV))
+    with pytest.raises(pm.PMError):
+        pm.normals_from_depth(d, K, out=torch.empty(2, 3, 96, 128, device=DEV, dtype=torch.float16))
+    # well-formed caller buffers are accepted and used
+    do = torch.empty_like(d)
+    _, _, pl = pm.process_frames(d, lab, K, 0.15, 0.03, 4, 8, 16, 0.01, 1, depth_out=do)
+    torch.cuda.synchronize()
+    assert pl.raw.shape == (2, 8, 12) and torch.isfinite(do).all()
+
+
+def test_host_pipeline_rejects_bad_arguments_before_copying(pm):
+    """pm_process_frames_host checks every argument before it
+    queues the first copy (and drains its streams on any exit), so a failed
+    call leaves nothing in flight and the next call works."""
+    d, lab, K = scenegen.stair_stream(0, 3, 128, 96, 8)
+    mm = torch.round(d.double() * 1000).to(torch.int32).to(torch.uint16).pin_memory()
+    lab8 = torch.where(lab < 0, torch.full_like(lab, 0xFF), lab).to(torch.uint8).pin_memory()
+    for bad in (dict(lam=0.3), dict(kappa=-1.0), dict(iters=-1), dict(n_hyp=0), dict(tau=0.0)):
+        kw = dict(lam=0.15, kappa=0.03, iters=20, n_hyp=16, tau=0.01)
+        kw.update(bad)
+        with pytest.raises(pm.PMError):
+            pm.process_frames_host(mm, lab8, K, kw["lam"], kw["kappa"], kw["iters"], 8, kw["n_hyp"], kw["tau"], 1,
+                                   chunk_frames=1)
+    good = pm.process_frames_host(mm, lab8, K, 0.15, 0.03, 20, 8, 16, 0.01, 1, chunk_frames=1)
+    dd = pm.depth_u16_to_metres(mm.cuda())
+    ref = pm.process_frames(dd, lab.cuda(), K, 0.15, 0.03, 20, 8, 16, 0.01, 1)[2]
+    torch.cuda.synchronize()
+    assert torch.equal(good.raw, ref.raw.cpu())
