@@ -175,6 +175,17 @@ PM_DEVINL void sweep_pairs(const float* __restrict__ cur, float* __restrict__ nx
         *reinterpret_cast<float2*>(ocol) = cellp(C, N, C, P);
 }
 
+#ifdef PM_ADF_TIMING
+// Per-phase SM-cycle counters of adf_pass_kernel (variant builds, tools/):
+// load+scan, sweeps, epilogue (stores / normals); [3] = plain, [4..6] fused.
+__device__ unsigned long long g_adf_prof[8];
+#define PM_ATS(v) const long long v = clock64()
+#define PM_AACC(k, a, b) if (threadIdx.x == 0) atomicAdd(&g_adf_prof[k], (unsigned long long)((b) - (a)))
+#else
+#define PM_ATS(v)
+#define PM_AACC(k, a, b)
+#endif
+
 template <int R>
 constexpr size_t pass_smem_bytes() { return sizeof(float) * ((size_t)2 * kSW * (kTH + 2 * R) + kSW); }
 
@@ -210,12 +221,14 @@ adf_pass_kernel(const float* __restrict__ src, float* __restrict__ dst, float* _
     b.ix0 = max(0, -x0); b.ix1 = min(kSW, W - x0);
     b.iy0 = max(0, -y0); b.iy1 = min(SH, H - y0);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    PM_ATS(t0);
 
     // load tile + halo: one TMA box (out-of-image cells zero-filled, never
     // read) or coalesced LDG rows; note whether every in-image pixel is valid
     // (fast path) or not (hole-aware path)
     bool all_valid = true;
     if (use_tma) {
+#ifndef PM_ADF_EXP_NOLOAD   // timing experiment only (wrong results): no tile load
         if (threadIdx.x == 0) mbar_init(&bar, 1);
         __syncthreads();
         if (threadIdx.x == 0) {
@@ -223,6 +236,10 @@ adf_pass_kernel(const float* __restrict__ src, float* __restrict__ dst, float* _
             tma_load_3d(buf0, &tmap, x0, y0, (int)frame, &bar);
         }
         mbar_wait(&bar, 0);
+#else
+        for (int i = threadIdx.x; i < kSW * SH; i += kThreads) buf0[i] = 1.0f + 1e-3f * (i & 7);
+        __syncthreads();
+#endif
         // validity scan (skipped when an earlier pass found the frame hole-free:
         // validity never changes, Q4): each lane checks 4 consecutive columns
         if (flag_mode != 2 || frame_flags[frame] != 0) {
@@ -255,9 +272,11 @@ adf_pass_kernel(const float* __restrict__ src, float* __restrict__ dst, float* _
     // the unchecked sweeps only where no update can turn a pixel invalid
     const bool fast = all_valid && !p.keep_valid;
 
+    const bool pairs = ((b.ix0 | b.ix1) & 1) == 0;
+
+    PM_ATS(t1);
     float* cur = buf0;
     float* nxt = buf1;
-    const bool pairs = ((b.ix0 | b.ix1) & 1) == 0;
     // Interior, hole-free tiles (the loaded region lies inside the image: ~55 %
     // of a 640x480 frame's tiles): the sweep geometry is a compile-time
     // constant -- sweeps unrolled, Box literal -- so the per-warp-sweep setup
@@ -293,6 +312,10 @@ adf_pass_kernel(const float* __restrict__ src, float* __restrict__ dst, float* _
 #undef PM_SWEEPS
     }
 
+    PM_ATS(t2);
+    [[maybe_unused]] const int pk_ = normals ? 4 : 0;
+    PM_AACC(pk_ + 0, t0, t1);
+    PM_AACC(pk_ + 1, t1, t2);
     // write the tile (and its normals).  Rows of float4 quads when W % 4 == 0
     // (the tile origin is then 16-byte aligned in global and shared memory).
     const int ox = blockIdx.x * TW, oy = blockIdx.y * kTH;
@@ -353,6 +376,8 @@ adf_pass_kernel(const float* __restrict__ src, float* __restrict__ dst, float* _
         if (!nrm) quads(F_{}, GEO{});
         else if (p.nmode == PM_NORMALS_AS_PRINTED) { if (nocheck) quads(F_{}, PRN{}); else quads(T_{}, PRN{}); }
         else { if (nocheck) quads(F_{}, GEO{}); else quads(T_{}, GEO{}); }
+        PM_ATS(t3);
+        PM_AACC(pk_ + 2, t2, t3);
         return;
     }
     for (int y = warp; y < kTH; y += kWarps) {
@@ -520,4 +545,14 @@ cudaError_t normals_run(const float* depth, float* normals, int W, int H, int B,
     return launch_pass(depth, nullptr, normals, W, H, B, 0, true, p, stream);
 }
 
+#ifdef PM_ADF_TIMING
+extern "C" __attribute__((visibility("default"))) int pm_debug_adf_prof(unsigned long long* out, int reset) {
+    if (cudaMemcpyFromSymbol(out, pm::g_adf_prof, sizeof(unsigned long long) * 8) != cudaSuccess) return 1;
+    if (reset) {
+        unsigned long long z[8] = {};
+        cudaMemcpyToSymbol(pm::g_adf_prof, z, sizeof(z));
+    }
+    return 0;
+}
+#endif
 }  // namespace pm

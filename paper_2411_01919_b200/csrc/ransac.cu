@@ -201,6 +201,14 @@ PM_DEVINL void count_lt(int& c, float a, float b) {
 #ifndef PM_SCORE_FADD_MASK
 #define PM_SCORE_FADD_MASK 0
 #endif
+// pairs j with bit (j mod 4) set count by the sign of fl(|d| - tau) (FADD on
+// the FMA pipe with the |.| operand modifier, then LEA.HI / shift-add of the
+// sign bit on the ALU pipe): fl(|d| - tau) < 0 exactly when |d| < tau (the
+// rounded difference keeps its sign and is +0 only at |d| == tau; |NaN| - tau
+// is a positive NaN), so the counts stay bit-exact.
+#ifndef PM_SCORE_SIGN_MASK
+#define PM_SCORE_SIGN_MASK 0
+#endif
 
 // Packed-pair scoring (two hypotheses per FFMA2 chain) for even K without the
 // error sum, reading the plane pairs the hyp kernel lays out (ws.pairs).
@@ -293,7 +301,10 @@ ransac_score_kernel(RansacWorkspace ws, RansacArgs a) {
                     asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(d) : "l"(Y[j]), "l"(py));
                     asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(d) : "l"(Z[j]), "l"(pz));
                     const float2 df = f2up(d);
-                    if (!((PM_SCORE_FADD_MASK >> (j & 3)) & 1)) {
+                    if ((PM_SCORE_SIGN_MASK >> (j & 3)) & 1) {
+                        c[2 * j] += (int)(__float_as_uint(__fsub_rn(fabsf(df.x), tau)) >> 31);
+                        c[2 * j + 1] += (int)(__float_as_uint(__fsub_rn(fabsf(df.y), tau)) >> 31);
+                    } else if (!((PM_SCORE_FADD_MASK >> (j & 3)) & 1)) {
                         // ALU-pipe count (FSETP + predicated IADD): the FMA pipe
                         // keeps the three FFMA2 of the distance
                         count_lt(c[2 * j], fabsf(df.x), tau);
