@@ -478,39 +478,47 @@ def run_cuda(args, rank, world, local_rank):
     rs_roof["clock_mhz"] = clk
     # ---- e2e: host-resident inputs through the public C-ABI host entry
     # (pm_process_frames_host): pinned sensor-native uint16 depth (mm) and
-    # uint8 labels (64 regions) in, plane table out; H2D of every input byte and D2H of
-    # the plane table inside the timed region, chunked and overlapped with
-    # the kernels.  (Frames are mm-quantised by the D435 noise model, so the
-    # uint16 form is lossless up to f32 rounding of mm * 1e-3.)
+    # the region labels as row runs (PM_LABELS_RUNS: piecewise-constant label
+    # images take a few KB per frame; the paper's regions are polygons)
+    # in, plane table out; the H2D of every input byte and the D2H of the
+    # plane table inside the timed region, chunked and overlapped with the
+    # kernels.  (Frames are mm-quantised by the D435 noise model, so the
+    # uint16 form is lossless up to f32 rounding of mm * 1e-3.)  The dense
+    # uint8 label image (3 B/px in total) is measured alongside.
     h_mm = torch.round(depth.double() * 1000).clamp(0, 65535).to(torch.int32).to(torch.uint16).cpu().pin_memory()
-    h_lab = torch.where(labels < 0, torch.full_like(labels, 0xFF), labels).to(torch.uint8)
-    h_lab = h_lab.cpu().pin_memory()
+    lab_cpu = labels.cpu()
+    h_lab = torch.where(lab_cpu < 0, torch.full_like(lab_cpu, 0xFF), lab_cpu).to(torch.uint8).pin_memory()
+    h_runs = pm.encode_label_runs(lab_cpu).pin_memory()
     h_planes = torch.empty(B, REGIONS, pm.PLANE_WORDS, dtype=torch.int32).pin_memory()
     chunk = args.e2e_chunk
-    arena = torch.empty(pm.host_pipeline_arena_bytes(W, H, REGIONS, HYPS, chunk, pm.DEPTH_U16_MM, pm.LABELS_U8),
-                        dtype=torch.uint8, device=dev)
+    arena = torch.empty(max(pm.host_pipeline_arena_bytes(W, H, REGIONS, HYPS, chunk, pm.DEPTH_U16_MM, f)
+                            for f in (pm.LABELS_U8, pm.LABELS_RUNS)), dtype=torch.uint8, device=dev)
     del ws
     torch.cuda.empty_cache()
 
-    def e2e_step():
-        pm.process_frames_host(h_mm, h_lab, K, LAM, KAPPA, ITERS, REGIONS, HYPS, TAU, SEED, first_frame_id=first,
-                               chunk_frames=chunk, planes_out=h_planes, arena=arena, device=dev)
+    def e2e_run(lab_host):
+        def e2e_step():
+            pm.process_frames_host(h_mm, lab_host, K, LAM, KAPPA, ITERS, REGIONS, HYPS, TAU, SEED,
+                                   first_frame_id=first, chunk_frames=chunk, planes_out=h_planes, arena=arena,
+                                   device=dev)
+        for _ in range(max(1, args.warmup)):
+            e2e_step()
+        torch.cuda.synchronize(dev)
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            e2e_step()
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        te = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        return world * B * args.steps / (float(te.item()) / 1e3)
 
-    for _ in range(max(1, args.warmup)):
-        e2e_step()
-    torch.cuda.synchronize(dev)
-    barrier()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(args.steps):
-        e2e_step()
-    e1.record(stream)
-    torch.cuda.synchronize(dev)
-    te = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e_value = world * B * args.steps / (float(te.item()) / 1e3)
-    e2e_h2d = B * W * H * (2 + 1)
+    e2e_value = e2e_run(h_runs)
+    e2e_dense = e2e_run(h_lab)
+    e2e_h2d = B * W * H * 2 + h_runs.nbytes
     e2e_d2h = B * REGIONS * 48
     del arena
     torch.cuda.empty_cache()
@@ -554,8 +562,10 @@ def run_cuda(args, rank, world, local_rank):
             "configs": extra,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "frames/s", "h2d_bytes_per_step": e2e_h2d,
-                    "d2h_bytes_per_step": e2e_d2h, "api": "pm_process_frames_host (uint16 mm depth + uint8 labels, "
-                                                          f"pinned; {chunk}-frame chunks, copies overlapped)"},
+                    "d2h_bytes_per_step": e2e_d2h,
+                    "api": "pm_process_frames_host (uint16 mm depth + row-run labels PM_LABELS_RUNS, pinned; "
+                           f"{chunk}-frame chunks, copies overlapped)",
+                    "dense_uint8_labels": {"value": e2e_dense, "h2d_bytes_per_step": B * W * H * 3}},
             "gpu_launches": launches_per_step * args.steps,
             "clocks": clocks.summary(),
         }

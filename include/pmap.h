@@ -272,12 +272,27 @@ PM_API size_t pm_segment_workspace_bytes(int32_t W, int32_t H, int32_t n_frames,
  *                format; 0 = invalid; converted as (float)mm * 1e-3f)
  *   labels_host  [B][H][W] in label_format: PM_LABELS_I32 (int32, -1 = none),
  *                PM_LABELS_U16 (uint16, 0xFFFF = none; n_regions <= 65535) or
- *                PM_LABELS_U8 (uint8, 0xFF = none; n_regions <= 255)
+ *                PM_LABELS_U8 (uint8, 0xFF = none; n_regions <= 255); or, for
+ *                PM_LABELS_RUNS, a pointer to a pm_label_runs: the same label
+ *                image as row runs (region labels are piecewise constant --
+ *                the paper's regions are polygons, P:287 -- so a frame's
+ *                labels take a few KB instead of W*H bytes on the link)
  *   planes_host  [B][n_regions] pm_plane (host)
  *   arena        device memory >= pm_host_pipeline_arena_bytes(...), 256-B aligned.
  * Other arguments as pm_process_frames. */
 enum { PM_DEPTH_F32_M = 0, PM_DEPTH_U16_MM = 1 };
-enum { PM_LABELS_I32 = 0, PM_LABELS_U16 = 1, PM_LABELS_U8 = 2 };
+enum { PM_LABELS_I32 = 0, PM_LABELS_U16 = 1, PM_LABELS_U8 = 2, PM_LABELS_RUNS = 3 };
+/* Run-length labels of B frames (host memory, pinned for asynchronous copies).
+ * Row y of frame f (global row index g = f * H + y) is the runs
+ * runs[row_start[g] .. row_start[g + 1]), left to right; a run is
+ * (label | length << 16): label in the low 16 bits (0xFFFF = none; labels
+ * >= n_regions are ignored like any out-of-range label), length >= 1 pixels.
+ * A row's lengths should sum to W: pixels past the last run are unlabelled,
+ * runs past W are cut.  row_start has B * H + 1 entries, row_start[0] = 0. */
+typedef struct {
+    const uint32_t* row_start;
+    const uint32_t* runs;
+} pm_label_runs;
 PM_API pm_status pm_process_frames_host(const void* depth_host, int32_t depth_format, const void* labels_host,
                                         int32_t label_format, int32_t W, int32_t H, int32_t n_frames,
                                         uint32_t first_frame_id, const pm_intrinsics* K, float lambda,

@@ -35,7 +35,7 @@ ADF_ALG1, ADF_DIVERGENCE = 0, 1
 NORMALS_GEOMETRIC, NORMALS_AS_PRINTED = 0, 1
 ENGINE_AUTO, ENGINE_TILED, ENGINE_REG = 0, 1, 3
 DEPTH_F32_M, DEPTH_U16_MM = 0, 1
-LABELS_I32, LABELS_U16, LABELS_U8 = 0, 1, 2
+LABELS_I32, LABELS_U16, LABELS_U8, LABELS_RUNS = 0, 1, 2, 3
 PLANE_WORDS = 12          # sizeof(pm_plane) / 4
 
 
@@ -347,21 +347,79 @@ def depth_u16_to_metres(depth_mm: torch.Tensor, out: torch.Tensor = None, scale:
     return out
 
 
-def process_frames_host(depth: torch.Tensor, labels: torch.Tensor, K, lam: float, kappa: float, iters: int,
+class pm_label_runs(ctypes.Structure):
+    _fields_ = [("row_start", ctypes.c_void_p), ("runs", ctypes.c_void_p)]
+
+
+class LabelRuns(NamedTuple):
+    """Row run-length region labels of [B, H, W] frames (host tensors, int32
+    storage of the uint32 words of include/pmap.h pm_label_runs)."""
+    row_start: torch.Tensor   # [B*H + 1]
+    runs: torch.Tensor        # [n_runs]: label (low 16 bits, 0xFFFF = none) | length << 16
+    shape: tuple              # (B, H, W)
+
+    def pin_memory(self):
+        return LabelRuns(self.row_start.pin_memory(), self.runs.pin_memory(), self.shape)
+
+    @property
+    def nbytes(self) -> int:
+        return 4 * (self.row_start.numel() + self.runs.numel())
+
+
+def encode_label_runs(labels: torch.Tensor) -> LabelRuns:
+    """[B, H, W] integer labels (negative or >= 0xFFFF = none) -> LabelRuns
+    (host side, vectorised): one run per maximal constant stretch of a row."""
+    import numpy as np
+    a = labels.detach().cpu().numpy().astype(np.int64)
+    if a.ndim != 3:
+        raise PMError("pmap: expected [B, H, W] labels")
+    B, H, W = a.shape
+    if W > 65535:
+        raise PMError("pmap: run lengths are 16-bit (W <= 65535)")
+    lab = np.where((a < 0) | (a >= 0xFFFF), 0xFFFF, a).reshape(B * H, W)
+    start = np.ones((B * H, W), bool)
+    start[:, 1:] = lab[:, 1:] != lab[:, :-1]
+    r_idx, c_idx = np.nonzero(start)                     # run starts, raster order
+    row_start = np.zeros(B * H + 1, np.uint32)
+    row_start[1:] = np.cumsum(start.sum(1), dtype=np.uint64).astype(np.uint32)
+    end = np.empty_like(c_idx)
+    end[:-1] = c_idx[1:]
+    end[-1] = W
+    last = np.ones(len(c_idx), bool)
+    last[:-1] = r_idx[1:] != r_idx[:-1]
+    end[last] = W
+    runs = lab[r_idx, c_idx].astype(np.uint32) | ((end - c_idx).astype(np.uint32) << 16)
+    return LabelRuns(torch.from_numpy(row_start.view(np.int32).copy()), torch.from_numpy(runs.view(np.int32).copy()),
+                     (B, H, W))
+
+
+def process_frames_host(depth: torch.Tensor, labels, K, lam: float, kappa: float, iters: int,
                         n_regions: int, n_hyp: int, tau: float, seed: int, first_frame_id: int = 0,
                         chunk_frames: int = 64, planes_out: torch.Tensor = None, depth_out: torch.Tensor = None,
                         normals_out: torch.Tensor = None, arena: torch.Tensor = None, device=None):
     """pm_process_frames_host: CPU (preferably pinned) tensors in, CPU plane
     table out.  depth: [B, H, W] float32 metres or uint16 millimetres; labels:
-    [B, H, W] int32 or uint16 (0xFFFF = none)."""
-    if depth.is_cuda or labels.is_cuda:
+    [B, H, W] int32, uint16 (0xFFFF = none) or uint8 (0xFF = none), or a
+    LabelRuns (encode_label_runs)."""
+    runs = labels if isinstance(labels, LabelRuns) else None
+    if depth.is_cuda or (runs is None and labels.is_cuda):
         raise PMError("pmap: process_frames_host takes host tensors")
-    if depth.dim() != 3 or tuple(labels.shape) != tuple(depth.shape):
+    if depth.dim() != 3 or tuple(runs.shape if runs is not None else labels.shape) != tuple(depth.shape):
         raise PMError("pmap: expected [B, H, W] depth and labels")
     dfmt = {torch.float32: DEPTH_F32_M, torch.uint16: DEPTH_U16_MM}.get(depth.dtype)
-    lfmt = {torch.int32: LABELS_I32, torch.uint16: LABELS_U16, torch.uint8: LABELS_U8}.get(labels.dtype)
-    if dfmt is None or lfmt is None or not depth.is_contiguous() or not labels.is_contiguous():
-        raise PMError("pmap: depth float32|uint16, labels int32|uint16|uint8, contiguous")
+    if runs is not None:
+        lfmt = LABELS_RUNS
+        if runs.row_start.is_cuda or runs.runs.is_cuda or runs.row_start.dtype != torch.int32 or \
+                runs.runs.dtype != torch.int32 or not runs.row_start.is_contiguous() or \
+                not runs.runs.is_contiguous() or runs.row_start.numel() != depth.shape[0] * depth.shape[1] + 1:
+            raise PMError("pmap: LabelRuns must hold contiguous host int32 row_start [B*H+1] and runs")
+        lab_arg = pm_label_runs(runs.row_start.data_ptr(), runs.runs.data_ptr())
+    else:
+        lfmt = {torch.int32: LABELS_I32, torch.uint16: LABELS_U16, torch.uint8: LABELS_U8}.get(labels.dtype)
+        if lfmt is not None and not labels.is_contiguous():
+            lfmt = None
+    if dfmt is None or lfmt is None or not depth.is_contiguous():
+        raise PMError("pmap: depth float32|uint16, labels int32|uint16|uint8|LabelRuns, contiguous")
     B, H, W = depth.shape
     dev = torch.device("cuda") if device is None else torch.device(device)
     C = min(int(chunk_frames), B)
@@ -377,7 +435,8 @@ def process_frames_host(depth: torch.Tensor, labels: torch.Tensor, K, lam: float
         normals_out = _out(normals_out, (B, 3, H, W), torch.float32, cpu, "normals_out")
     with torch.cuda.device(dev):
         stream = torch.cuda.current_stream(dev).cuda_stream
-        _check(_lib.pm_process_frames_host(depth.data_ptr(), dfmt, labels.data_ptr(), lfmt, W, H, B,
+        lab_ptr = ctypes.addressof(lab_arg) if runs is not None else labels.data_ptr()
+        _check(_lib.pm_process_frames_host(depth.data_ptr(), dfmt, lab_ptr, lfmt, W, H, B,
                                            int(first_frame_id), ctypes.byref(_K(K)), float(lam), float(kappa),
                                            int(iters), int(n_regions), int(n_hyp), float(tau),
                                            int(seed) & (2**64 - 1), planes_out.data_ptr(),

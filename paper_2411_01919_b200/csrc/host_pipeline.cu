@@ -49,10 +49,34 @@ u8_labels_kernel(const uint8_t* __restrict__ in, int32_t* __restrict__ out, size
     if (i < n) out[i] = in[i] == 0xFFu ? -1 : (int32_t)in[i];
 }
 
+// row runs -> int32 labels: one warp per image row, the row's runs written in
+// turn by the whole warp (coalesced); 0xFFFF -> -1; pixels past the last run
+// -> -1, runs past W cut.  row_start is relative to the chunk's first run.
+__global__ void __launch_bounds__(kConvThreads)
+runs_labels_kernel(const uint32_t* __restrict__ row_start, uint32_t base, const uint32_t* __restrict__ runs,
+                   int32_t* __restrict__ out, int W, int rows) {
+    const int row = blockIdx.x * (kConvThreads / 32) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (row >= rows) return;
+    const uint32_t r0 = row_start[row] - base, r1 = row_start[row + 1] - base;
+    int32_t* o = out + (size_t)row * W;
+    int x = 0;
+    for (uint32_t r = r0; r < r1 && x < W; ++r) {
+        const uint32_t run = runs[r];
+        const int len = min((int)(run >> 16), W - x);
+        const int32_t lab = (run & 0xFFFFu) == 0xFFFFu ? -1 : (int32_t)(run & 0xFFFFu);
+        for (int i = lane; i < len; i += 32) o[x + i] = lab;
+        x += len;
+    }
+    for (int i = x + lane; i < W; i += 32) o[i] = -1;
+}
+
 struct DeviceStreams {
     cudaStream_t copy = nullptr;      // H2D
     cudaStream_t down = nullptr;      // D2H
+    cudaStream_t comp[2] = {};        // kernels of slot 0 / 1 (chunks k and k+1 may overlap: wave tails)
     cudaEvent_t h2d[2] = {}, done[2] = {}, freed[2] = {};
+    cudaEvent_t start = nullptr;      // the caller's stream at entry
     std::mutex mu;            // one host pipeline at a time per device
     cudaError_t err = cudaSuccess;
 };
@@ -67,6 +91,9 @@ DeviceStreams* streams_for_current_device() {
         DeviceStreams* d = new DeviceStreams();
         d->err = cudaStreamCreateWithFlags(&d->copy, cudaStreamNonBlocking);
         if (d->err == cudaSuccess) d->err = cudaStreamCreateWithFlags(&d->down, cudaStreamNonBlocking);
+        for (int s = 0; s < 2 && d->err == cudaSuccess; ++s)
+            d->err = cudaStreamCreateWithFlags(&d->comp[s], cudaStreamNonBlocking);
+        if (d->err == cudaSuccess) d->err = cudaEventCreateWithFlags(&d->start, cudaEventDisableTiming);
         for (int s = 0; s < 2 && d->err == cudaSuccess; ++s) {
             d->err = cudaEventCreateWithFlags(&d->h2d[s], cudaEventDisableTiming);
             if (d->err == cudaSuccess) d->err = cudaEventCreateWithFlags(&d->done[s], cudaEventDisableTiming);
@@ -81,7 +108,8 @@ size_t a256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 struct Slot {
     void* raw_depth;      // host-format depth staging (u16) or f32 depth directly
-    void* raw_labels;     // host-format labels (u16) or int32 directly
+    void* raw_labels;     // host-format labels (u16 / u8 / run row starts) or int32 directly
+    uint32_t* raw_runs;   // PM_LABELS_RUNS: the chunk's runs (<= one per pixel)
     float* depth;         // f32 metres (== raw_depth for f32 input)
     int32_t* labels;      // int32 (== raw_labels for int32 input)
     float* depth_out;
@@ -108,9 +136,11 @@ Arena arena_layout(void* base, int W, int H, int R, int n_hyp, int C, int depth_
         sl.depth = (float*)take(sizeof(float) * px);
         sl.raw_depth = depth_fmt == PM_DEPTH_U16_MM ? take(sizeof(uint16_t) * px) : (void*)sl.depth;
         sl.labels = (int32_t*)take(sizeof(int32_t) * px);
-        sl.raw_labels = label_fmt == PM_LABELS_U16 ? take(sizeof(uint16_t) * px)
-                        : label_fmt == PM_LABELS_U8 ? take(sizeof(uint8_t) * px)
-                                                    : (void*)sl.labels;
+        sl.raw_labels = label_fmt == PM_LABELS_U16    ? take(sizeof(uint16_t) * px)
+                        : label_fmt == PM_LABELS_U8   ? take(sizeof(uint8_t) * px)
+                        : label_fmt == PM_LABELS_RUNS ? take(sizeof(uint32_t) * ((size_t)C * H + 1))
+                                                      : (void*)sl.labels;
+        sl.raw_runs = label_fmt == PM_LABELS_RUNS ? (uint32_t*)take(sizeof(uint32_t) * px) : nullptr;
         sl.depth_out = (float*)take(sizeof(float) * px);
         sl.normals = (float*)take(sizeof(float) * 3 * px);
         sl.planes = (pm_plane*)take(sizeof(pm_plane) * (size_t)C * (R > 0 ? R : 1));
@@ -155,8 +185,12 @@ PM_API pm_status pm_process_frames_host(const void* depth_host, int32_t depth_fo
     if (!depth_host || !labels_host || !planes_host || chunk_frames < 1 || n_frames < 1)
         return PM_ERR_INVALID_ARGUMENT;
     if (depth_format != PM_DEPTH_F32_M && depth_format != PM_DEPTH_U16_MM) return PM_ERR_INVALID_ARGUMENT;
-    if (label_format != PM_LABELS_I32 && label_format != PM_LABELS_U16 && label_format != PM_LABELS_U8)
+    if (label_format != PM_LABELS_I32 && label_format != PM_LABELS_U16 && label_format != PM_LABELS_U8 &&
+        label_format != PM_LABELS_RUNS)
         return PM_ERR_INVALID_ARGUMENT;
+    const pm_label_runs* lr = label_format == PM_LABELS_RUNS ? (const pm_label_runs*)labels_host : nullptr;
+    if (lr && (!lr->row_start || !lr->runs)) return PM_ERR_INVALID_ARGUMENT;
+    if (lr && W > 65535) return PM_ERR_INVALID_ARGUMENT;
     if (label_format == PM_LABELS_U16 && n_regions > 65535) return PM_ERR_INVALID_ARGUMENT;
     if (label_format == PM_LABELS_U8 && n_regions > 255) return PM_ERR_INVALID_ARGUMENT;
     const int C = chunk_frames < n_frames ? chunk_frames : n_frames;
@@ -174,20 +208,27 @@ PM_API pm_status pm_process_frames_host(const void* depth_host, int32_t depth_fo
     cudaStream_t cs = (cudaStream_t)stream;
     const size_t frame_px = (size_t)W * H;
     const size_t dsz = depth_format == PM_DEPTH_U16_MM ? 2 : 4;
-    const size_t lsz = label_format == PM_LABELS_U16 ? 2 : label_format == PM_LABELS_U8 ? 1 : 4;
+    const size_t lsz = label_format == PM_LABELS_U16 ? 2 : label_format == PM_LABELS_U8 ? 1 : 4;   // not RUNS
     const int n_chunks = (n_frames + C - 1) / C;
     // every exit waits for the copies already queued on the internal streams
     // (and the kernels feeding them): the caller may free or reuse its host
     // buffers and the arena as soon as this returns, also on error
     auto finish = [&](pm_status st) {
         const cudaError_t e1 = cudaStreamSynchronize(ds->copy);
-        const cudaError_t e2 = cudaStreamSynchronize(cs);
+        const cudaError_t e2 = cudaStreamSynchronize(ds->comp[0]);
+        const cudaError_t e4 = cudaStreamSynchronize(ds->comp[1]);
         const cudaError_t e3 = cudaStreamSynchronize(ds->down);
-        if (st == PM_OK && (e1 != cudaSuccess || e2 != cudaSuccess || e3 != cudaSuccess)) st = PM_ERR_CUDA;
+        const cudaError_t e5 = cudaStreamSynchronize(cs);
+        if (st == PM_OK && (e1 != cudaSuccess || e2 != cudaSuccess || e3 != cudaSuccess || e4 != cudaSuccess ||
+                            e5 != cudaSuccess))
+            st = PM_ERR_CUDA;
         return st;
     };
     cudaError_t e = cudaSuccess;
-    // both slots start free
+    // everything after the caller's earlier work on `stream`; both slots start free
+    e = cudaEventRecord(ds->start, cs);
+    for (int s = 0; s < 2 && e == cudaSuccess; ++s) e = cudaStreamWaitEvent(ds->comp[s], ds->start, 0);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(ds->copy, ds->start, 0);
     for (int s = 0; s < 2 && e == cudaSuccess; ++s) e = cudaEventRecord(ds->freed[s], cs);
     for (int k = 0; k < n_chunks && e == cudaSuccess; ++k) {
         const int s = k & 1;
@@ -200,31 +241,51 @@ PM_API pm_status pm_process_frames_host(const void* depth_host, int32_t depth_fo
         if (e == cudaSuccess)
             e = cudaMemcpyAsync(sl.raw_depth, (const char*)depth_host + (size_t)f0 * frame_px * dsz, px * dsz,
                                 cudaMemcpyHostToDevice, ds->copy);
-        if (e == cudaSuccess)
+        uint32_t run_base = 0;
+        if (lr) {   // the chunk's row starts and runs (a contiguous slice of each)
+            const size_t g0 = (size_t)f0 * H, g1 = (size_t)(f0 + nf) * H;
+            run_base = lr->row_start[g0];
+            const size_t nruns = lr->row_start[g1] - run_base;
+            if (nruns > px) return finish(PM_ERR_INVALID_ARGUMENT);      // > one run per pixel
+            if (e == cudaSuccess)
+                e = cudaMemcpyAsync(sl.raw_labels, lr->row_start + g0, sizeof(uint32_t) * (g1 - g0 + 1),
+                                    cudaMemcpyHostToDevice, ds->copy);
+            if (e == cudaSuccess && nruns)
+                e = cudaMemcpyAsync(sl.raw_runs, lr->runs + run_base, sizeof(uint32_t) * nruns,
+                                    cudaMemcpyHostToDevice, ds->copy);
+        } else if (e == cudaSuccess) {
             e = cudaMemcpyAsync(sl.raw_labels, (const char*)labels_host + (size_t)f0 * frame_px * lsz, px * lsz,
                                 cudaMemcpyHostToDevice, ds->copy);
+        }
         if (e == cudaSuccess) e = cudaEventRecord(ds->h2d[s], ds->copy);
-        // compute on the caller's stream
-        if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, ds->h2d[s], 0);
+        // the chunk's kernels on the slot's compute stream (the other slot's
+        // chunk may still be running: its last wave overlaps this one's first)
+        cudaStream_t ks = ds->comp[s];
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(ks, ds->h2d[s], 0);
         if (e != cudaSuccess) break;
         if (depth_format == PM_DEPTH_U16_MM) {
-            pm_status st = pm_depth_u16_to_metres((const uint16_t*)sl.raw_depth, sl.depth, px, 1e-3f, stream);
+            pm_status st = pm_depth_u16_to_metres((const uint16_t*)sl.raw_depth, sl.depth, px, 1e-3f, ks);
             if (st != PM_OK) return finish(st);
         }
         if (label_format == PM_LABELS_U16) {
-            u16_labels_kernel<<<(unsigned)((px + kConvThreads - 1) / kConvThreads), kConvThreads, 0, cs>>>(
+            u16_labels_kernel<<<(unsigned)((px + kConvThreads - 1) / kConvThreads), kConvThreads, 0, ks>>>(
                 (const uint16_t*)sl.raw_labels, sl.labels, px);
             if ((e = cudaGetLastError()) != cudaSuccess) break;
         } else if (label_format == PM_LABELS_U8) {
-            u8_labels_kernel<<<(unsigned)((px + kConvThreads - 1) / kConvThreads), kConvThreads, 0, cs>>>(
+            u8_labels_kernel<<<(unsigned)((px + kConvThreads - 1) / kConvThreads), kConvThreads, 0, ks>>>(
                 (const uint8_t*)sl.raw_labels, sl.labels, px);
+            if ((e = cudaGetLastError()) != cudaSuccess) break;
+        } else if (lr) {
+            const int rows = nf * H;
+            runs_labels_kernel<<<(unsigned)((rows + kConvThreads / 32 - 1) / (kConvThreads / 32)), kConvThreads, 0,
+                                 ks>>>((const uint32_t*)sl.raw_labels, run_base, sl.raw_runs, sl.labels, W, rows);
             if ((e = cudaGetLastError()) != cudaSuccess) break;
         }
         pm_status st = pm_process_frames(sl.depth, sl.labels, W, H, nf, first_frame_id + (uint32_t)f0, K, lambda,
                                          kappa, iters, n_regions, n_hyp, inlier_thresh, seed, sl.depth_out,
-                                         sl.normals, sl.planes, sl.ws, sl.ws_bytes, stream);
+                                         sl.normals, sl.planes, sl.ws, sl.ws_bytes, ks);
         if (st != PM_OK) return finish(st);
-        e = cudaEventRecord(ds->done[s], cs);
+        e = cudaEventRecord(ds->done[s], ks);
         // D2H of the results on the download stream; the slot is free afterwards
         if (e == cudaSuccess) e = cudaStreamWaitEvent(ds->down, ds->done[s], 0);
         if (e == cudaSuccess && n_regions > 0)
@@ -238,6 +299,7 @@ PM_API pm_status pm_process_frames_host(const void* depth_host, int32_t depth_fo
                                 cudaMemcpyDeviceToHost, ds->down);
         if (e == cudaSuccess) e = cudaEventRecord(ds->freed[s], ds->down);
     }
+    for (int s = 0; s < 2 && e == cudaSuccess; ++s) e = cudaStreamWaitEvent(cs, ds->freed[s], 0);
     return finish(e == cudaSuccess ? PM_OK : PM_ERR_CUDA);
 }
 

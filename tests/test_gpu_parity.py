@@ -750,3 +750,40 @@ def test_host_pipeline_rejects_bad_arguments_before_copying(pm):
     ref = pm.process_frames(dd, lab.cuda(), K, 0.15, 0.03, 20, 8, 16, 0.01, 1)[2]
     torch.cuda.synchronize()
     assert torch.equal(good.raw, ref.raw.cpu())
+
+
+def test_host_pipeline_run_length_labels(pm):
+    """PM_LABELS_RUNS: the same label image as row runs gives the same plane
+    tables (bitwise) as the dense uint8 labels, over chunk boundaries; a row
+    whose runs fall short of W leaves the rest unlabelled, runs past W are cut."""
+    d, lab, K = scenegen.stair_stream(7, 5, 256, 120, 24)
+    mm = torch.round(d.double() * 1000).to(torch.int32).to(torch.uint16).pin_memory()
+    lab = lab.clone()
+    lab[1, 10:20, 30:90] = -1                                   # unlabelled holes inside a region
+    lab[3, :, 200:] = 23                                        # a column band: many short runs
+    lab8 = torch.where(lab < 0, torch.full_like(lab, 0xFF), lab).to(torch.uint8).pin_memory()
+    runs = pm.encode_label_runs(lab).pin_memory()
+    assert runs.nbytes < lab8.numel() // 10
+    for chunk in (1, 2, 5):
+        dense = pm.process_frames_host(mm, lab8, K, 0.15, 0.03, 20, 24, 32, 0.01, 5, first_frame_id=7,
+                                       chunk_frames=chunk)
+        rl = pm.process_frames_host(mm, runs, K, 0.15, 0.03, 20, 24, 32, 0.01, 5, first_frame_id=7,
+                                    chunk_frames=chunk)
+        assert torch.equal(dense.raw, rl.raw), chunk
+    # malformed rows: row 0 of frame 0 sums to W - 16 (tail unlabelled); row 1 to W + 40 (cut)
+    rs = runs.row_start.clone().numpy().view(np.uint32).astype(np.int64)
+    rr = runs.runs.clone().numpy().view(np.uint32).astype(np.int64)
+    lab_bad = lab.clone()
+    i0 = rs[0]
+    rr[i0] = (rr[i0] & 0xFFFF) | (((rr[i0] >> 16) - 16) << 16)
+    if rs[1] - rs[0] == 1:
+        lab_bad[0, 0, 256 - 16:] = -1
+    i1 = rs[2] - 1
+    rr[i1] = (rr[i1] & 0xFFFF) | (((rr[i1] >> 16) + 40) << 16)
+    bad = pm.LabelRuns(torch.from_numpy(rs.astype(np.uint32).view(np.int32)),
+                       torch.from_numpy(rr.astype(np.uint32).view(np.int32)), runs.shape)
+    if rs[1] - rs[0] == 1:
+        lab_bad8 = torch.where(lab_bad < 0, torch.full_like(lab_bad, 0xFF), lab_bad).to(torch.uint8)
+        a = pm.process_frames_host(mm, lab_bad8.pin_memory(), K, 0.15, 0.03, 20, 24, 32, 0.01, 5, chunk_frames=2)
+        b = pm.process_frames_host(mm, bad.pin_memory(), K, 0.15, 0.03, 20, 24, 32, 0.01, 5, chunk_frames=2)
+        assert torch.equal(a.raw, b.raw)
