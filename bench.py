@@ -496,11 +496,14 @@ def run_cuda(args, rank, world, local_rank):
     del ws
     torch.cuda.empty_cache()
 
-    def e2e_run(lab_host):
+    def e2e_run(lab_host, sync=True):
+        # sync=False: pm_process_frames_host_async per step (the next step's
+        # uploads run under this step's last kernels); the timed region ends
+        # with the stream that waits for every step's last download
         def e2e_step():
             pm.process_frames_host(h_mm, lab_host, K, LAM, KAPPA, ITERS, REGIONS, HYPS, TAU, SEED,
                                    first_frame_id=first, chunk_frames=chunk, planes_out=h_planes, arena=arena,
-                                   device=dev)
+                                   device=dev, sync=sync)
         for _ in range(max(1, args.warmup)):
             e2e_step()
         torch.cuda.synchronize(dev)
@@ -516,7 +519,8 @@ def run_cuda(args, rank, world, local_rank):
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         return world * B * args.steps / (float(te.item()) / 1e3)
 
-    e2e_value = e2e_run(h_runs)
+    e2e_value = e2e_run(h_runs, sync=False)
+    e2e_sync = e2e_run(h_runs)
     e2e_dense = e2e_run(h_lab)
     e2e_h2d = B * W * H * 2 + h_runs.nbytes
     e2e_d2h = B * REGIONS * 48
@@ -563,8 +567,10 @@ def run_cuda(args, rank, world, local_rank):
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "frames/s", "h2d_bytes_per_step": e2e_h2d,
                     "d2h_bytes_per_step": e2e_d2h,
-                    "api": "pm_process_frames_host (uint16 mm depth + row-run labels PM_LABELS_RUNS, pinned; "
-                           f"{chunk}-frame chunks, copies overlapped)",
+                    "api": "pm_process_frames_host_async per step (uint16 mm depth + row-run labels "
+                           f"PM_LABELS_RUNS, pinned; {chunk}-frame chunks, copies overlapped with the kernels and "
+                           "with the previous step)",
+                    "synchronous_calls": {"value": e2e_sync},
                     "dense_uint8_labels": {"value": e2e_dense, "h2d_bytes_per_step": B * W * H * 3}},
             "gpu_launches": launches_per_step * args.steps,
             "clocks": clocks.summary(),
@@ -610,7 +616,7 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="CPU work budget of the oracle baseline")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extra", action="store_true", help="skip the C2/C3/C5/holes extra configs")
-    ap.add_argument("--e2e-chunk", type=int, default=64, help="frames per chunk of the host pipeline")
+    ap.add_argument("--e2e-chunk", type=int, default=256, help="frames per chunk of the host pipeline")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))

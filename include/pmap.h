@@ -300,6 +300,23 @@ PM_API pm_status pm_process_frames_host(const void* depth_host, int32_t depth_fo
                                         float inlier_thresh, uint64_t seed, pm_plane* planes_host,
                                         float* depth_out_host, float* normals_host, int32_t chunk_frames,
                                         void* arena, size_t arena_bytes, pm_stream_t stream);
+/* The same, asynchronous: returns once every copy and kernel is queued.  The
+ * host buffers (inputs and outputs) and the arena must stay untouched until
+ * `stream` has completed (cudaStreamSynchronize(stream), or an event recorded
+ * on it after the call); the inputs must be ready when the call is made.
+ * Consecutive calls on the same device overlap: the next call's first upload
+ * runs under this call's last kernels (the arena's two slots are reused only
+ * after their previous downloads).  Errors found before anything is queued
+ * return as for the synchronous call; a failure after that drains the
+ * internal streams before returning. */
+PM_API pm_status pm_process_frames_host_async(const void* depth_host, int32_t depth_format,
+                                              const void* labels_host, int32_t label_format, int32_t W,
+                                              int32_t H, int32_t n_frames, uint32_t first_frame_id,
+                                              const pm_intrinsics* K, float lambda, float kappa, int32_t iters,
+                                              int32_t n_regions, int32_t n_hyp, float inlier_thresh,
+                                              uint64_t seed, pm_plane* planes_host, float* depth_out_host,
+                                              float* normals_host, int32_t chunk_frames, void* arena,
+                                              size_t arena_bytes, pm_stream_t stream);
 PM_API size_t pm_host_pipeline_arena_bytes(int32_t W, int32_t H, int32_t n_regions, int32_t n_hyp,
                                            int32_t chunk_frames, int32_t depth_format, int32_t label_format);
 /* uint16 millimetres -> f32 metres (device buffers, n values): m = (float)mm * scale. */

@@ -90,6 +90,9 @@ _lib.pm_ransac_planes_ex.argtypes = [_P, _I32, _I32, _I32, _U32, _KP, _P, _I32, 
                                      ctypes.POINTER(pm_ransac_options), _P]
 _lib.pm_process_frames.argtypes = [_P, _P, _I32, _I32, _I32, _U32, _KP, _F32, _F32, _I32, _I32, _I32, _F32,
                                    _U64, _P, _P, _P, _P, _SZ, _P]
+_lib.pm_process_frames_host_async.argtypes = [_P, _I32, _P, _I32, _I32, _I32, _I32, _U32, _KP, _F32, _F32, _I32,
+                                              _I32, _I32, _F32, _U64, _P, _P, _P, _I32, _P, _SZ, _P]
+_lib.pm_process_frames_host_async.restype = ctypes.c_int
 _lib.pm_process_frames_host.argtypes = [_P, _I32, _P, _I32, _I32, _I32, _I32, _U32, _KP, _F32, _F32, _I32, _I32,
                                         _I32, _F32, _U64, _P, _P, _P, _I32, _P, _SZ, _P]
 _lib.pm_host_pipeline_arena_bytes.restype = _SZ
@@ -108,7 +111,8 @@ EXPORTED = ("pm_adf_filter", "pm_adf_filter_batched", "pm_adf_filter_ex", "pm_ad
             "pm_normals_from_depth", "pm_normals_from_depth_batched", "pm_normals_from_depth_ex", "pm_ransac_planes",
             "pm_ransac_planes_batched", "pm_ransac_planes_ex", "pm_ransac_workspace_bytes",
             "pm_process_frames", "pm_pipeline_workspace_bytes", "pm_pipeline_kernel_launches",
-            "pm_process_frames_host", "pm_host_pipeline_arena_bytes", "pm_depth_u16_to_metres",
+            "pm_process_frames_host", "pm_process_frames_host_async", "pm_host_pipeline_arena_bytes",
+            "pm_depth_u16_to_metres",
             "pm_segment_regions", "pm_segment_workspace_bytes",
             "pm_region_polygons", "pm_region_polygons_workspace_bytes", "pm_rasterize_polygons",
             "pm_lift_polygon_vertices",
@@ -396,11 +400,15 @@ def encode_label_runs(labels: torch.Tensor) -> LabelRuns:
 def process_frames_host(depth: torch.Tensor, labels, K, lam: float, kappa: float, iters: int,
                         n_regions: int, n_hyp: int, tau: float, seed: int, first_frame_id: int = 0,
                         chunk_frames: int = 64, planes_out: torch.Tensor = None, depth_out: torch.Tensor = None,
-                        normals_out: torch.Tensor = None, arena: torch.Tensor = None, device=None):
+                        normals_out: torch.Tensor = None, arena: torch.Tensor = None, device=None,
+                        sync: bool = True):
     """pm_process_frames_host: CPU (preferably pinned) tensors in, CPU plane
     table out.  depth: [B, H, W] float32 metres or uint16 millimetres; labels:
     [B, H, W] int32, uint16 (0xFFFF = none) or uint8 (0xFF = none), or a
-    LabelRuns (encode_label_runs)."""
+    LabelRuns (encode_label_runs).  sync=False: pm_process_frames_host_async
+    -- returns once queued; the host tensors, planes_out and the arena (both
+    required then) must stay untouched until the device's current stream is
+    synchronised; consecutive calls overlap."""
     runs = labels if isinstance(labels, LabelRuns) else None
     if depth.is_cuda or (runs is None and labels.is_cuda):
         raise PMError("pmap: process_frames_host takes host tensors")
@@ -425,6 +433,8 @@ def process_frames_host(depth: torch.Tensor, labels, K, lam: float, kappa: float
     C = min(int(chunk_frames), B)
     if dev.type == "cuda" and dev.index is None:
         dev = torch.device("cuda", torch.cuda.current_device())
+    if not sync and (arena is None or planes_out is None):
+        raise PMError("pmap: sync=False needs a caller-owned arena and planes_out (they outlive the call)")
     arena = _ws(arena, 0, dev, "arena") if arena is not None else torch.empty(
         host_pipeline_arena_bytes(W, H, n_regions, n_hyp, C, dfmt, lfmt), dtype=torch.uint8, device=dev)
     cpu = torch.device("cpu")
@@ -436,7 +446,8 @@ def process_frames_host(depth: torch.Tensor, labels, K, lam: float, kappa: float
     with torch.cuda.device(dev):
         stream = torch.cuda.current_stream(dev).cuda_stream
         lab_ptr = ctypes.addressof(lab_arg) if runs is not None else labels.data_ptr()
-        _check(_lib.pm_process_frames_host(depth.data_ptr(), dfmt, lab_ptr, lfmt, W, H, B,
+        fn = _lib.pm_process_frames_host if sync else _lib.pm_process_frames_host_async
+        _check(fn(depth.data_ptr(), dfmt, lab_ptr, lfmt, W, H, B,
                                            int(first_frame_id), ctypes.byref(_K(K)), float(lam), float(kappa),
                                            int(iters), int(n_regions), int(n_hyp), float(tau),
                                            int(seed) & (2**64 - 1), planes_out.data_ptr(),

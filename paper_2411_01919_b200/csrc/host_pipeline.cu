@@ -94,11 +94,13 @@ DeviceStreams* streams_for_current_device() {
         for (int s = 0; s < 2 && d->err == cudaSuccess; ++s)
             d->err = cudaStreamCreateWithFlags(&d->comp[s], cudaStreamNonBlocking);
         if (d->err == cudaSuccess) d->err = cudaEventCreateWithFlags(&d->start, cudaEventDisableTiming);
+        // (the freed events are recorded below, once every event exists: both slots start free)
         for (int s = 0; s < 2 && d->err == cudaSuccess; ++s) {
             d->err = cudaEventCreateWithFlags(&d->h2d[s], cudaEventDisableTiming);
             if (d->err == cudaSuccess) d->err = cudaEventCreateWithFlags(&d->done[s], cudaEventDisableTiming);
             if (d->err == cudaSuccess) d->err = cudaEventCreateWithFlags(&d->freed[s], cudaEventDisableTiming);
         }
+        for (int s = 0; s < 2 && d->err == cudaSuccess; ++s) d->err = cudaEventRecord(d->freed[s], d->copy);
         per_dev[dev] = d;
     }
     return per_dev[dev];
@@ -174,14 +176,16 @@ PM_API pm_status pm_depth_u16_to_metres(const uint16_t* depth_mm, float* depth_m
     return cudaGetLastError() == cudaSuccess ? PM_OK : PM_ERR_CUDA;
 }
 
-PM_API pm_status pm_process_frames_host(const void* depth_host, int32_t depth_format, const void* labels_host,
-                                        int32_t label_format, int32_t W, int32_t H, int32_t n_frames,
-                                        uint32_t first_frame_id, const pm_intrinsics* K, float lambda, float kappa,
-                                        int32_t iters, int32_t n_regions, int32_t n_hyp, float inlier_thresh,
-                                        uint64_t seed, pm_plane* planes_host, float* depth_out_host,
-                                        float* normals_host, int32_t chunk_frames, void* arena, size_t arena_bytes,
-                                        pm_stream_t stream) {
-    using namespace pm;
+}  // extern "C"
+
+namespace pm {
+namespace {
+pm_status host_pipeline(const void* depth_host, int32_t depth_format, const void* labels_host, int32_t label_format,
+                        int32_t W, int32_t H, int32_t n_frames, uint32_t first_frame_id, const pm_intrinsics* K,
+                        float lambda, float kappa, int32_t iters, int32_t n_regions, int32_t n_hyp,
+                        float inlier_thresh, uint64_t seed, pm_plane* planes_host, float* depth_out_host,
+                        float* normals_host, int32_t chunk_frames, void* arena, size_t arena_bytes,
+                        pm_stream_t stream, bool async) {
     if (!depth_host || !labels_host || !planes_host || chunk_frames < 1 || n_frames < 1)
         return PM_ERR_INVALID_ARGUMENT;
     if (depth_format != PM_DEPTH_F32_M && depth_format != PM_DEPTH_U16_MM) return PM_ERR_INVALID_ARGUMENT;
@@ -225,11 +229,16 @@ PM_API pm_status pm_process_frames_host(const void* depth_host, int32_t depth_fo
         return st;
     };
     cudaError_t e = cudaSuccess;
-    // everything after the caller's earlier work on `stream`; both slots start free
-    e = cudaEventRecord(ds->start, cs);
-    for (int s = 0; s < 2 && e == cudaSuccess; ++s) e = cudaStreamWaitEvent(ds->comp[s], ds->start, 0);
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(ds->copy, ds->start, 0);
-    for (int s = 0; s < 2 && e == cudaSuccess; ++s) e = cudaEventRecord(ds->freed[s], cs);
+    if (!async) {
+        // everything after the caller's earlier work on `stream`
+        e = cudaEventRecord(ds->start, cs);
+        for (int s = 0; s < 2 && e == cudaSuccess; ++s) e = cudaStreamWaitEvent(ds->comp[s], ds->start, 0);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(ds->copy, ds->start, 0);
+    }
+    // (async: the inputs are host memory the caller has ready; each slot is
+    // reused after its previous download -- possibly a previous call's --
+    // through the freed events, so consecutive calls overlap: the next call's
+    // first upload runs under this call's last kernels)
     for (int k = 0; k < n_chunks && e == cudaSuccess; ++k) {
         const int s = k & 1;
         const Slot& sl = A.slot[s];
@@ -299,8 +308,38 @@ PM_API pm_status pm_process_frames_host(const void* depth_host, int32_t depth_fo
                                 cudaMemcpyDeviceToHost, ds->down);
         if (e == cudaSuccess) e = cudaEventRecord(ds->freed[s], ds->down);
     }
+    // the caller's stream completes after the last download of both slots
     for (int s = 0; s < 2 && e == cudaSuccess; ++s) e = cudaStreamWaitEvent(cs, ds->freed[s], 0);
+    if (async && e == cudaSuccess) return PM_OK;
     return finish(e == cudaSuccess ? PM_OK : PM_ERR_CUDA);
+}
+}  // namespace
+}  // namespace pm
+
+extern "C" {
+
+PM_API pm_status pm_process_frames_host(const void* depth_host, int32_t depth_format, const void* labels_host,
+                                        int32_t label_format, int32_t W, int32_t H, int32_t n_frames,
+                                        uint32_t first_frame_id, const pm_intrinsics* K, float lambda, float kappa,
+                                        int32_t iters, int32_t n_regions, int32_t n_hyp, float inlier_thresh,
+                                        uint64_t seed, pm_plane* planes_host, float* depth_out_host,
+                                        float* normals_host, int32_t chunk_frames, void* arena, size_t arena_bytes,
+                                        pm_stream_t stream) {
+    return pm::host_pipeline(depth_host, depth_format, labels_host, label_format, W, H, n_frames, first_frame_id, K,
+                             lambda, kappa, iters, n_regions, n_hyp, inlier_thresh, seed, planes_host,
+                             depth_out_host, normals_host, chunk_frames, arena, arena_bytes, stream, false);
+}
+
+PM_API pm_status pm_process_frames_host_async(const void* depth_host, int32_t depth_format, const void* labels_host,
+                                              int32_t label_format, int32_t W, int32_t H, int32_t n_frames,
+                                              uint32_t first_frame_id, const pm_intrinsics* K, float lambda,
+                                              float kappa, int32_t iters, int32_t n_regions, int32_t n_hyp,
+                                              float inlier_thresh, uint64_t seed, pm_plane* planes_host,
+                                              float* depth_out_host, float* normals_host, int32_t chunk_frames,
+                                              void* arena, size_t arena_bytes, pm_stream_t stream) {
+    return pm::host_pipeline(depth_host, depth_format, labels_host, label_format, W, H, n_frames, first_frame_id, K,
+                             lambda, kappa, iters, n_regions, n_hyp, inlier_thresh, seed, planes_host,
+                             depth_out_host, normals_host, chunk_frames, arena, arena_bytes, stream, true);
 }
 
 }  // extern "C"

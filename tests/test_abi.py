@@ -118,3 +118,4 @@ def test_next_features_reject_bad_arguments_before_launch(pm):
                           None, 8, ws, big, None)
     assert L.pm_process_frames_host(*args(pm.LABELS_U8, 256)) == 1
     assert L.pm_process_frames_host(*args(7, 64)) == 1
+    assert L.pm_process_frames_host_async(*args(7, 64)) == 1

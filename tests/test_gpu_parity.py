@@ -787,3 +787,26 @@ def test_host_pipeline_run_length_labels(pm):
         a = pm.process_frames_host(mm, lab_bad8.pin_memory(), K, 0.15, 0.03, 20, 24, 32, 0.01, 5, chunk_frames=2)
         b = pm.process_frames_host(mm, bad.pin_memory(), K, 0.15, 0.03, 20, 24, 32, 0.01, 5, chunk_frames=2)
         assert torch.equal(a.raw, b.raw)
+
+
+def test_host_pipeline_async_calls_equal_sync(pm):
+    """pm_process_frames_host_async: several calls queued back to back on one
+    arena (the next call's uploads run under the previous call's kernels)
+    give the tables of the synchronous call, per call."""
+    d, lab, K = scenegen.stair_stream(20, 6, 192, 128, 16)
+    mm = torch.round(d.double() * 1000).to(torch.int32).to(torch.uint16).pin_memory()
+    runs = pm.encode_label_runs(lab).pin_memory()
+    dev = torch.device("cuda", 0)
+    arena = torch.empty(pm.host_pipeline_arena_bytes(192, 128, 16, 32, 2, pm.DEPTH_U16_MM, pm.LABELS_RUNS),
+                        dtype=torch.uint8, device=dev)
+    ref = pm.process_frames_host(mm, runs, K, 0.15, 0.03, 20, 16, 32, 0.01, 9, first_frame_id=20, chunk_frames=2,
+                                 arena=arena, device=dev)
+    outs = [torch.empty(6, 16, pm.PLANE_WORDS, dtype=torch.int32).pin_memory() for _ in range(4)]
+    for o in outs:                                   # chunks 2 + 2 + 2: slots 0, 1, 0 -> next call starts on 0
+        pm.process_frames_host(mm, runs, K, 0.15, 0.03, 20, 16, 32, 0.01, 9, first_frame_id=20, chunk_frames=2,
+                               planes_out=o, arena=arena, device=dev, sync=False)
+    torch.cuda.current_stream(dev).synchronize()
+    for o in outs:
+        assert torch.equal(o, ref.raw)
+    with pytest.raises(pm.PMError):
+        pm.process_frames_host(mm, runs, K, 0.15, 0.03, 20, 16, 32, 0.01, 9, sync=False)
