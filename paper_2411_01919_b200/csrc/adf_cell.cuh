@@ -193,8 +193,6 @@ PM_DEVINL bool fast_depth(float z) { return (__float_as_uint(z) - 0x0D800000u) <
 // ---- adf_reg.cu (register-tile engine), host side
 constexpr int kMaxItersRegPass = 16;
 cudaError_t adf_reg_setup_attributes();
-// true when a pass of `sweeps` sweeps (+ normals) over src can run on the register engine
-bool adf_reg_applicable(const float* src, int W, int H, int B, int sweeps, bool normals);
 // Launches one pass on the register engine when applicable (*launched = true);
 // otherwise returns cudaSuccess with *launched = false and launches nothing.
 cudaError_t adf_reg_pass(const float* src, float* dst, float* normals, int W, int H, int B, int sweeps,

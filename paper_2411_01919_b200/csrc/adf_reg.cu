@@ -668,12 +668,6 @@ cudaError_t adf_reg_setup_attributes() {
     return cudaSuccess;
 }
 
-bool adf_reg_applicable(const float* src, int W, int H, int B, int sweeps, bool normals) {
-    RegGeom G;
-    if (((uintptr_t)src & 15u) != 0 || sweeps > kMaxItersRegPass) return false;
-    return make_geom(W, H, B, sweeps, normals, G);
-}
-
 cudaError_t adf_reg_pass(const float* src, float* dst, float* normals, int W, int H, int B, int sweeps,
                          const AdfParams& p, cudaStream_t stream, int* frame_flags, int flag_mode, bool* launched) {
     *launched = false;

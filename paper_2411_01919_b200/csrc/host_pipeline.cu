@@ -54,11 +54,12 @@ u8_labels_kernel(const uint8_t* __restrict__ in, int32_t* __restrict__ out, size
 // -> -1, runs past W cut.  row_start is relative to the chunk's first run.
 __global__ void __launch_bounds__(kConvThreads)
 runs_labels_kernel(const uint32_t* __restrict__ row_start, uint32_t base, const uint32_t* __restrict__ runs,
-                   int32_t* __restrict__ out, int W, int rows) {
+                   uint32_t nruns, int32_t* __restrict__ out, int W, int rows) {
     const int row = blockIdx.x * (kConvThreads / 32) + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
     if (row >= rows) return;
-    const uint32_t r0 = row_start[row] - base, r1 = row_start[row + 1] - base;
+    // a malformed (non-monotonic) row_start never reads past the chunk's runs
+    const uint32_t r0 = min(row_start[row] - base, nruns), r1 = min(row_start[row + 1] - base, nruns);
     int32_t* o = out + (size_t)row * W;
     int x = 0;
     for (uint32_t r = r0; r < r1 && x < W; ++r) {
@@ -250,12 +251,13 @@ pm_status host_pipeline(const void* depth_host, int32_t depth_format, const void
         if (e == cudaSuccess)
             e = cudaMemcpyAsync(sl.raw_depth, (const char*)depth_host + (size_t)f0 * frame_px * dsz, px * dsz,
                                 cudaMemcpyHostToDevice, ds->copy);
-        uint32_t run_base = 0;
+        uint32_t run_base = 0, run_count = 0;
         if (lr) {   // the chunk's row starts and runs (a contiguous slice of each)
             const size_t g0 = (size_t)f0 * H, g1 = (size_t)(f0 + nf) * H;
             run_base = lr->row_start[g0];
             const size_t nruns = lr->row_start[g1] - run_base;
             if (nruns > px) return finish(PM_ERR_INVALID_ARGUMENT);      // > one run per pixel
+            run_count = (uint32_t)nruns;
             if (e == cudaSuccess)
                 e = cudaMemcpyAsync(sl.raw_labels, lr->row_start + g0, sizeof(uint32_t) * (g1 - g0 + 1),
                                     cudaMemcpyHostToDevice, ds->copy);
@@ -287,7 +289,8 @@ pm_status host_pipeline(const void* depth_host, int32_t depth_format, const void
         } else if (lr) {
             const int rows = nf * H;
             runs_labels_kernel<<<(unsigned)((rows + kConvThreads / 32 - 1) / (kConvThreads / 32)), kConvThreads, 0,
-                                 ks>>>((const uint32_t*)sl.raw_labels, run_base, sl.raw_runs, sl.labels, W, rows);
+                                 ks>>>((const uint32_t*)sl.raw_labels, run_base, sl.raw_runs, run_count, sl.labels, W,
+                                       rows);
             if ((e = cudaGetLastError()) != cudaSuccess) break;
         }
         pm_status st = pm_process_frames(sl.depth, sl.labels, W, H, nf, first_frame_id + (uint32_t)f0, K, lambda,
