@@ -12,7 +12,7 @@
 
 namespace {
 
-constexpr int32_t kVersion = 100;   // 0.1.0
+constexpr int32_t kVersion = 200;   // 0.2.0: pm_ransac_options.stage_events, PM_LABELS_RUNS, pm_process_frames_host_async, PM_ADF_ENGINE_REG
 
 // Kernel attributes (> 48 KB dynamic shared memory) are per device context:
 // set once per device, on first use from any thread.
