@@ -427,8 +427,8 @@ PM_API int32_t pm_pipeline_kernel_launches(int32_t iters, int32_t n_regions);
 
 /* Human-readable status. */
 PM_API const char* pm_status_string(pm_status s);
-/* ABI version (major * 10000 + minor * 100 + patch). */
-/* 100 * major + minor.  0.2.0 (200): pm_ransac_options gained stage_events
+/* ABI version (major * 10000 + minor * 100 + patch).  0.2.0 (200):
+ * pm_ransac_options gained stage_events
  * (a caller built against 0.1 passes a shorter struct -- rebuild), PM_LABELS_RUNS,
  * pm_process_frames_host_async, PM_ADF_ENGINE_REG; engine value 2 removed. */
 PM_API int32_t pm_version(void);
