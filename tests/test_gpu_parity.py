@@ -810,3 +810,20 @@ def test_host_pipeline_async_calls_equal_sync(pm):
         assert torch.equal(o, ref.raw)
     with pytest.raises(pm.PMError):
         pm.process_frames_host(mm, runs, K, 0.15, 0.03, 20, 16, 32, 0.01, 9, sync=False)
+
+
+def test_two_devices_in_one_process(pm):
+    """Per-device setup (the kernels' shared-memory attributes are set once per
+    device context): process_frames on a second GPU of the same process equals
+    the first GPU's result bit for bit.  Needs two visible devices."""
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs two CUDA devices")
+    d, lab, K = scenegen.stair_stream(0, 2, 128, 96, 16)
+    res = []
+    for i in (0, 1):
+        dev = torch.device("cuda", i)
+        out = pm.process_frames(d.to(dev), lab.to(dev), K, 0.15, 0.03, 20, 16, 64, 0.01, 7)
+        torch.cuda.synchronize(dev)
+        res.append([t.raw.cpu() if hasattr(t, "raw") else t.cpu() for t in out])
+    for a, b in zip(*res):
+        assert torch.equal(a, b)
