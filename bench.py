@@ -345,8 +345,21 @@ def extra_configs(pm, dev, clk_mhz, hbm_peak):
     bb = bufs(B, H, W, REGIONS, HYPS)
     ms = _time_pipeline(pm, d, lab, K, ITERS, REGIONS, HYPS, 0, 5, 2, bb)
     st = stage_times(pm, d, lab, K, ITERS, REGIONS, HYPS, 0, bb[3], bb[0], bb[1], bb[2], reps=3)
+    # the same frames through the opt-in PM_ADF_ENGINE_HOLES (fix-up walk), ADF stage alone
+    hf = lambda: pm.adf_filter(d, K, LAM, KAPPA, ITERS, out=bb[0], normals_out=bb[1], workspace=bb[3],
+                               engine=pm.ENGINE_HOLES)
+    for _ in range(2):
+        hf()
+    e0, e1 = _events(2)
+    e0.record()
+    for _ in range(5):
+        hf()
+    e1.record()
+    torch.cuda.synchronize()
     res["C4_holes_1pct"] = {"value": B / (ms / 1e3), "unit": "frames/s", "frames_per_step": B, "ms_per_step": ms,
-                            "stages_ms": st, "workload": "C4 stream with 1 % hash-selected dropout holes per frame"}
+                            "stages_ms": st, "adf_normals_ms_engine_holes": e0.elapsed_time(e1) / 5,
+                            "workload": "C4 stream with 1 % hash-selected dropout holes per frame (default engine; "
+                                        "adf_normals_ms_engine_holes: the ADF stage with PM_ADF_ENGINE_HOLES)"}
     del d, lab, bb
     torch.cuda.empty_cache()
 

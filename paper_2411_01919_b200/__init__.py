@@ -33,7 +33,7 @@ SAMPLER_PHILOX, SAMPLER_ENUMERATE = 0, 1
 SELECT_COUNT, SELECT_ERROR = 0, 1
 ADF_ALG1, ADF_DIVERGENCE = 0, 1
 NORMALS_GEOMETRIC, NORMALS_AS_PRINTED = 0, 1
-ENGINE_AUTO, ENGINE_TILED, ENGINE_REG = 0, 1, 3
+ENGINE_AUTO, ENGINE_TILED, ENGINE_REG, ENGINE_HOLES = 0, 1, 3, 4
 DEPTH_F32_M, DEPTH_U16_MM = 0, 1
 LABELS_I32, LABELS_U16, LABELS_U8, LABELS_RUNS = 0, 1, 2, 3
 PLANE_WORDS = 12          # sizeof(pm_plane) / 4

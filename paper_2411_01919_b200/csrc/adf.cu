@@ -51,6 +51,17 @@ constexpr int kSW = 128;
 // shared memory for R <= 5 (the default passes), and 480-row frames split
 // into 11 tiles wasting 4 rows (64-row tiles: 8 tiles, 32 wasted rows).
 constexpr int kTH = 44;
+// Hole lists: one per warp of the validity scan, kWarpHoles uint16 entries
+// each, in the 512-B spare row.  A tile takes the fix-up path when every warp's
+// list fits and the 5 stencil cells of all its holes fit 2 per thread
+// (<= 102 invalid cells, ~1.5 % of a 52-row tile); otherwise the checked walk.
+constexpr int kWarpHoles = kSW * 2 / kWarps;
+constexpr int kFixItems = 2;
+constexpr int kHoleCap = kFixItems * kThreads / 5;
+// Per-tile record of the first pass's hole lists (list_mode 1 writes, 2
+// reads): 8 uint16 counts, then the 512-B lists -- kListVecs + 1 uint4.
+constexpr int kListVecs = kSW * 2 * 2 / 16;
+PM_DEVINL size_t tile_index() { return ((size_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x; }
 
 struct Box { int ix0, ix1, iy0, iy1; };
 
@@ -199,19 +210,28 @@ __host__ __device__ constexpr int tile_w() { return kSW - 2 * halo_x<R>(); }
 
 // One pass of `iters` sweeps; halo R = iters (+1 when the normals are fused).
 //   src [B][H][W] -> dst [B][H][W] (if dst) and normals [B][3][H][W] (if normals).
-template <int R, bool DIV>
+// FIX (PM_ADF_ENGINE_HOLES): tiles with a few holes run the unchecked walk
+// plus the fix-up of the cells next to a hole (below) instead of the checked
+// walk.  Its bookkeeping stays out of the FIX = false kernels, which are the
+// default: it costs the hole-free tiles 1-4 %.
+template <int R, bool DIV, bool FIX>
 __global__ void __launch_bounds__(kThreads, 4)   // <= 64 registers: 4 CTAs / SM
 adf_pass_kernel(const float* __restrict__ src, float* __restrict__ dst, float* __restrict__ normals,
                 int W, int H, int iters, AdfParams p, const __grid_constant__ CUtensorMap tmap, int use_tma,
-                int* __restrict__ frame_flags, int flag_mode) {
+                int* __restrict__ frame_flags, int flag_mode, uint4* __restrict__ tile_lists, int list_mode) {
     constexpr int SH = kTH + 2 * R;
     constexpr int RA = halo_x<R>();
     constexpr int TW = tile_w<R>();
     constexpr int PAD = RA - R;
     extern __shared__ __align__(128) float smem[];
     __shared__ __align__(8) uint64_t bar;
+    __shared__ int s_wn[kWarps];               // invalid cells found by each warp's scan
     float* buf0 = smem;
     float* buf1 = smem + kSW * SH;
+    // hole lists (smem (sy << 7) | sx of the invalid in-image cells, warp w's
+    // at [w * kWarpHoles, ...)) in the spare row after buf1: the walks'
+    // one-row-ahead prefetch reads that row but never uses it, nothing writes it
+    uint16_t* hl = reinterpret_cast<uint16_t*>(smem + 2 * kSW * SH);
     const size_t frame = blockIdx.z;
     const size_t HW = (size_t)H * W;
     const float* in = src + frame * HW;
@@ -227,6 +247,7 @@ adf_pass_kernel(const float* __restrict__ src, float* __restrict__ dst, float* _
     // read) or coalesced LDG rows; note whether every in-image pixel is valid
     // (fast path) or not (hole-aware path)
     bool all_valid = true;
+    int wn = 0;                                // this warp's invalid cells (warp-uniform)
     if (use_tma) {
 #ifndef PM_ADF_EXP_NOLOAD   // timing experiment only (wrong results): no tile load
         if (threadIdx.x == 0) mbar_init(&bar, 1);
@@ -241,16 +262,49 @@ adf_pass_kernel(const float* __restrict__ src, float* __restrict__ dst, float* _
         __syncthreads();
 #endif
         // validity scan (skipped when an earlier pass found the frame hole-free:
-        // validity never changes, Q4): each lane checks 4 consecutive columns
-        if (flag_mode != 2 || frame_flags[frame] != 0) {
-            const int c0 = 4 * lane;
+        // validity never changes, Q4): each lane checks 4 consecutive columns.
+        // Passes with the first pass's tile geometry read that pass's hole
+        // lists instead (list_mode 2; loads overlap the tile load).
+        if (FIX && flag_mode == 2 && list_mode == 2) {
+            if (frame_flags[frame] != 0 && threadIdx.x <= kListVecs) {
+                const uint4 v = tile_lists[tile_index() * (kListVecs + 1) + threadIdx.x];
+                if (threadIdx.x == 0) {
+                    const uint32_t c[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                    for (int w = 0; w < kWarps; ++w) s_wn[w] = (int)((c[w >> 1] >> (16 * (w & 1))) & 0xFFFFu);
+                } else {
+                    reinterpret_cast<uint4*>(hl)[threadIdx.x - 1] = v;
+                }
+            } else if (threadIdx.x < kWarps) {
+                s_wn[threadIdx.x] = 0;
+            }
+        } else if (flag_mode != 2 || frame_flags[frame] != 0) {
+            const int c0 = 4 * lane;  // (4 columns per lane: 32 lanes cover the 128-column tile)
             bool in[4];
 #pragma unroll
             for (int j = 0; j < 4; ++j) in[j] = c0 + j >= b.ix0 && c0 + j < b.ix1;
             for (int sy = b.iy0 + warp; sy < b.iy1; sy += kWarps) {
                 const float4 v = *reinterpret_cast<const float4*>(buf0 + sy * kSW + c0);
-                all_valid &= (fast_depth(v.x) || !in[0]) && (fast_depth(v.y) || !in[1]) &&
-                             (fast_depth(v.z) || !in[2]) && (fast_depth(v.w) || !in[3]);
+                if constexpr (!FIX) {
+                    all_valid &= (fast_depth(v.x) || !in[0]) && (fast_depth(v.y) || !in[1]) &&
+                                 (fast_depth(v.z) || !in[2]) && (fast_depth(v.w) || !in[3]);
+                    continue;
+                }
+                const unsigned bad = (fast_depth(v.x) || !in[0] ? 0u : 1u) | (fast_depth(v.y) || !in[1] ? 0u : 2u) |
+                                     (fast_depth(v.z) || !in[2] ? 0u : 4u) | (fast_depth(v.w) || !in[3] ? 0u : 8u);
+                all_valid &= bad == 0;
+                // rare (warp-uniform branch): append the row's invalid cells to
+                // the warp's list, lanes ranked by ballot, one cell per lane per round
+                if (__any_sync(0xffffffffu, bad != 0)) {
+                    unsigned m = bad;
+                    for (unsigned any = __ballot_sync(0xffffffffu, m != 0); any;
+                         any = __ballot_sync(0xffffffffu, m != 0)) {
+                        const int k = wn + __popc(any & ((1u << lane) - 1u));
+                        if (m && k < kWarpHoles) hl[warp * kWarpHoles + k] = (uint16_t)((sy << 7) | (c0 + __ffs(m) - 1));
+                        m &= m - 1;
+                        wn += __popc(any);
+                    }
+                }
             }
         }
     } else {
@@ -267,10 +321,63 @@ adf_pass_kernel(const float* __restrict__ src, float* __restrict__ dst, float* _
             }
         }
     }
+    if constexpr (FIX) {
+        // (the row-load path keeps no lists: its hole tiles take the checked walk)
+        if (!use_tma) wn = __any_sync(0xffffffffu, !all_valid) ? kWarpHoles + 1 : 0;
+        if (lane == 0 && !(flag_mode == 2 && list_mode == 2)) s_wn[warp] = wn;
+    }
     all_valid = __syncthreads_and(all_valid);
     if (flag_mode == 1 && !all_valid && threadIdx.x == 0) atomicOr(frame_flags + frame, 1);
+    // tiles with a few holes: the unchecked walk everywhere, then the cells
+    // whose stencil touches a listed cell (the cell itself and its 4
+    // neighbours) recomputed with the checked cell -- every other cell's
+    // unchecked result is the checked one (all five operands fast_depth)
+    int pre[kWarps + 1] = {};                  // prefix of the per-warp counts
+    int wmax = 0;
+    if (FIX && (!all_valid || (flag_mode == 2 && list_mode == 2))) {
+#pragma unroll
+        for (int w = 0; w < kWarps; ++w) {
+            const int c = s_wn[w];
+            pre[w + 1] = pre[w] + c;
+            wmax = max(wmax, c);
+        }
+    }
+    const int nh = pre[kWarps];
+    if (FIX && flag_mode == 2 && list_mode == 2) all_valid = nh == 0;
+    else if (FIX && list_mode == 1 && threadIdx.x <= (all_valid ? 0 : kListVecs)) {   // keep them for the later passes
+        uint4 v;
+        if (threadIdx.x == 0) {
+            uint32_t c[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                c[j] = (uint32_t)min(s_wn[2 * j], 0xFFFF) | ((uint32_t)min(s_wn[2 * j + 1], 0xFFFF) << 16);
+            v = make_uint4(c[0], c[1], c[2], c[3]);
+        } else {
+            v = reinterpret_cast<const uint4*>(hl)[threadIdx.x - 1];
+        }
+        tile_lists[tile_index() * (kListVecs + 1) + threadIdx.x] = v;
+    }
     // the unchecked sweeps only where no update can turn a pixel invalid
     const bool fast = all_valid && !p.keep_valid;
+    const bool fixup = FIX && !all_valid && !p.keep_valid && nh <= kHoleCap && wmax <= kWarpHoles;
+    // this thread's stencil cells (items k = tid + 256 r of the 5 * nh: a
+    // listed cell and its 4 neighbours) as smem indices (sy << 7 | sx), -1 =
+    // none; fixed for the pass (holes never move)
+    int item[kFixItems];
+#pragma unroll
+    for (int r = 0; r < kFixItems; ++r) {
+        item[r] = -1;
+        const int k = threadIdx.x + r * kThreads;
+        if (fixup && k < 5 * nh) {
+            int h = k / 5;
+            const int d = k - 5 * h;
+            int w = 0;
+            while (h >= s_wn[w]) h -= s_wn[w++];
+            const int e = hl[w * kWarpHoles + h];
+            item[r] = e + (d == 1 ? -kSW : d == 2 ? kSW : d == 3 ? -1 : d == 4 ? 1 : 0);
+            if ((d == 3 && (e & 127) == 0) || (d == 4 && (e & 127) == kSW - 1)) item[r] = -1;
+        }
+    }
 
     const bool pairs = ((b.ix0 | b.ix1) & 1) == 0;
 
@@ -282,6 +389,27 @@ adf_pass_kernel(const float* __restrict__ src, float* __restrict__ dst, float* _
     // constant -- sweeps unrolled, Box literal -- so the per-warp-sweep setup
     // (row split, clipping, border offsets) folds to a few instructions.  Same
     // cells, same operands, same order: bitwise the generic loop's result.
+    // after sweep t's walk: the checked cell (border rule of the walks: an
+    // out-of-image neighbour is the centre) at this thread's stencil cells in
+    // the sweep region
+    auto fix = [&](int t) {
+        __syncthreads();                              // the walk's stores first
+        const int ylo = max(t, b.iy0), yhi = min(SH - t, b.iy1);
+        const int xlo = max(PAD + t, b.ix0), xhi = min(kSW - PAD - t, b.ix1);
+#pragma unroll
+        for (int r = 0; r < kFixItems; ++r) {
+            const int e = item[r];
+            const int sy = e >> 7, sx = e & 127;
+            if (e < 0 || sy < ylo || sy >= yhi || sx < xlo || sx >= xhi) continue;
+            const float* c = cur + e;
+            const float C = c[0];
+            const float N = sy == b.iy0 ? C : c[-kSW];
+            const float S = sy == b.iy1 - 1 ? C : c[kSW];
+            const float Wv = sx == b.ix0 ? C : c[-1];
+            const float E = sx == b.ix1 - 1 ? C : c[1];
+            nxt[e] = cell<true, DIV>(C, N, S, Wv, E, p);
+        }
+    };
     bool done = false;
     if constexpr (R <= 6) {
         if (fast && b.ix0 == 0 && b.ix1 == kSW && b.iy0 == 0 && b.iy1 == SH) {
@@ -306,9 +434,15 @@ adf_pass_kernel(const float* __restrict__ src, float* __restrict__ dst, float* _
         }
     };
     if (!done) {
-#define PM_SWEEPS(FN, CK) sweeps([&](int t) { FN<SH, PAD, CK, DIV>(cur, nxt, t, b, p); })
-        if (pairs) { if (fast) PM_SWEEPS(sweep_pairs, false); else PM_SWEEPS(sweep_pairs, true); }
-        else { if (fast) PM_SWEEPS(sweep, false); else PM_SWEEPS(sweep, true); }
+        // (the fix-up tiles share the unchecked walk's code: one copy of each walk)
+#define PM_SWEEPS(FN, CK) sweeps([&](int t) { FN<SH, PAD, CK, DIV>(cur, nxt, t, b, p); if (FIX && !CK && fixup) fix(t); })
+        if constexpr (FIX) {
+            if (pairs) { if (fast || fixup) PM_SWEEPS(sweep_pairs, false); else PM_SWEEPS(sweep_pairs, true); }
+            else { if (fast || fixup) PM_SWEEPS(sweep, false); else PM_SWEEPS(sweep, true); }
+        } else {
+            if (pairs) { if (fast) PM_SWEEPS(sweep_pairs, false); else PM_SWEEPS(sweep_pairs, true); }
+            else { if (fast) PM_SWEEPS(sweep, false); else PM_SWEEPS(sweep, true); }
+        }
 #undef PM_SWEEPS
     }
 
@@ -408,13 +542,16 @@ adf_pass_kernel(const float* __restrict__ src, float* __restrict__ dst, float* _
     }
 }
 
-using PassFn = void (*)(const float*, float*, float*, int, int, int, AdfParams, const CUtensorMap, int, int*, int);
+using PassFn = void (*)(const float*, float*, float*, int, int, int, AdfParams, const CUtensorMap, int, int*, int,
+                        uint4*, int);
 
 template <int R>
 struct PassTable {
-    static void fill(PassFn (*fns)[2], size_t* smem, int* tw) {
-        fns[R][0] = adf_pass_kernel<R, false>;
-        fns[R][1] = adf_pass_kernel<R, true>;
+    static void fill(PassFn (*fns)[2][2], size_t* smem, int* tw) {
+        fns[R][0][0] = adf_pass_kernel<R, false, false>;
+        fns[R][1][0] = adf_pass_kernel<R, true, false>;
+        fns[R][0][1] = adf_pass_kernel<R, false, true>;
+        fns[R][1][1] = adf_pass_kernel<R, true, true>;
         smem[R] = pass_smem_bytes<R>();
         tw[R] = tile_w<R>();
         PassTable<R - 1>::fill(fns, smem, tw);
@@ -422,11 +559,11 @@ struct PassTable {
 };
 template <>
 struct PassTable<0> {
-    static void fill(PassFn (*)[2], size_t*, int*) {}
+    static void fill(PassFn (*)[2][2], size_t*, int*) {}
 };
 
 struct Passes {
-    PassFn fn[kMaxItersPerPass + 2][2] = {};   // [R][scheme == PM_ADF_DIVERGENCE]
+    PassFn fn[kMaxItersPerPass + 2][2][2] = {};   // [R][scheme == PM_ADF_DIVERGENCE][FIX]
     size_t smem[kMaxItersPerPass + 2] = {};
     int tw[kMaxItersPerPass + 2] = {};
     Passes() { PassTable<kMaxItersPerPass + 1>::fill(fn, smem, tw); }
@@ -441,17 +578,19 @@ const Passes& passes() {
 cudaError_t adf_setup_attributes() {
     const Passes& P = passes();
     for (int R = 1; R <= kMaxItersPerPass + 1; ++R)
-        for (int d = 0; d < 2; ++d) {
-            cudaError_t e = cudaFuncSetAttribute(P.fn[R][d], cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 (int)P.smem[R]);
-            if (e != cudaSuccess) return e;
-        }
+        for (int d = 0; d < 2; ++d)
+            for (int f = 0; f < 2; ++f) {
+                cudaError_t e = cudaFuncSetAttribute(P.fn[R][d][f], cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                     (int)P.smem[R]);
+                if (e != cudaSuccess) return e;
+            }
     return cudaSuccess;
 }
 
 static cudaError_t launch_pass(const float* src, float* dst, float* normals, int W, int H, int B,
                                int iters, bool fuse, const AdfParams& p, cudaStream_t stream,
-                               int* frame_flags = nullptr, int flag_mode = 0) {
+                               int* frame_flags = nullptr, int flag_mode = 0, uint4* tile_lists = nullptr,
+                               int list_mode = 0, bool fix = false) {
     const int R = iters + (fuse ? 1 : 0);
     const Passes& P = passes();
     const int TW = P.tw[R];
@@ -461,14 +600,23 @@ static cudaError_t launch_pass(const float* src, float* dst, float* normals, int
     if (!use_tma) memset(&tmap, 0, sizeof(tmap));
     void* args[] = {(void*)&src,  (void*)&dst,  (void*)&normals, (void*)&W,           (void*)&H,
                     (void*)&iters, (void*)&p,   (void*)&tmap,    (void*)&use_tma,     (void*)&frame_flags,
-                    (void*)&flag_mode};
-    return cudaLaunchKernel((const void*)P.fn[R][p.scheme == PM_ADF_DIVERGENCE ? 1 : 0], grid, dim3(kThreads), args,
-                            P.smem[R], stream);
+                    (void*)&flag_mode, (void*)&tile_lists, (void*)&list_mode};
+    return cudaLaunchKernel((const void*)P.fn[R][p.scheme == PM_ADF_DIVERGENCE ? 1 : 0][fix ? 1 : 0], grid,
+                            dim3(kThreads), args, P.smem[R], stream);
 }
 
 int adf_default_iters_per_pass() { return 4; }
 
 size_t adf_flags_offset(int W, int H, int B) { return (sizeof(float) * (size_t)B * W * H + 255) & ~(size_t)255; }
+
+// the hole-list records after the flags: one per tile of the narrowest
+// plain-pass tiling (tile_w<kMaxItersPerPass>() = 96 columns)
+static size_t adf_lists_offset(int B) { return ((sizeof(int) * (size_t)B + 255) & ~(size_t)255); }
+size_t adf_flags_region_bytes(int W, int H, int B) {
+    const size_t tiles = (size_t)((W + tile_w<kMaxItersPerPass>() - 1) / tile_w<kMaxItersPerPass>()) *
+                         ((H + kTH - 1) / kTH) * B;
+    return (adf_lists_offset(B) + tiles * (kListVecs + 1) * sizeof(uint4) + 255) & ~(size_t)255;
+}
 
 static AdfParams make_params(const pm_intrinsics* K, float lam, float kappa, int scheme, int nmode) {
     AdfParams p;
@@ -517,11 +665,19 @@ cudaError_t adf_run(const float* in, float* out, float* normals, float* ws, int 
     int done = 0;
     // the register engine is opt-in: measured slower than the tiled engine on B200
     const bool try_reg = engine == PM_ADF_ENGINE_REG;
+    const bool fix = engine == PM_ADF_ENGINE_HOLES;   // the tiled engine with the fix-up walk
+    bool lists_written = false;   // by a tiled first pass
     for (int k = 0; k < passes; ++k) {
         const int it = (iters - done) / (passes - k);   // near-equal split, sums to iters
         float* dst = (((passes - 1 - k) & 1) == 0) ? out : ws;   // the last pass lands in `out`
         const bool last = k == passes - 1;
         const int mode = flags ? (k == 0 ? 1 : 2) : 0;
+        // hole lists: written by the first pass, read by the later plain
+        // passes that use its tile geometry (same sweep count, not fused)
+        const int it0 = iters / passes;
+        const bool fused = last && normals != nullptr;
+        int lmode = !flags || !fix ? 0 : k == 0 ? (fused ? 0 : 1) : (!fused && it == it0 && lists_written ? 2 : 0);
+        uint4* lists = flags ? reinterpret_cast<uint4*>(reinterpret_cast<char*>(flags) + adf_lists_offset(B)) : nullptr;
         bool launched = false;
         if (try_reg) {
             cudaError_t e = adf_reg_pass(src, dst, last ? normals : nullptr, W, H, B, it, p, stream, flags, mode,
@@ -529,9 +685,10 @@ cudaError_t adf_run(const float* in, float* out, float* normals, float* ws, int 
             if (e != cudaSuccess) return e;
         }
         if (!launched) {
-            cudaError_t e = launch_pass(src, dst, last ? normals : nullptr, W, H, B, it, last && normals != nullptr,
-                                        p, stream, flags, mode);
+            cudaError_t e = launch_pass(src, dst, last ? normals : nullptr, W, H, B, it, fused, p, stream, flags,
+                                        mode, lists, lmode, fix);
             if (e != cudaSuccess) return e;
+            if (lmode == 1) lists_written = true;
         }
         src = dst;
         done += it;

@@ -12,7 +12,7 @@
 
 namespace {
 
-constexpr int32_t kVersion = 200;   // 0.2.0: pm_ransac_options.stage_events, PM_LABELS_RUNS, pm_process_frames_host_async, PM_ADF_ENGINE_REG
+constexpr int32_t kVersion = 200;   // 0.2.0: pm_ransac_options.stage_events, PM_LABELS_RUNS, pm_process_frames_host_async, PM_ADF_ENGINE_REG / _HOLES
 
 // Kernel attributes (> 48 KB dynamic shared memory) are per device context:
 // set once per device, on first use from any thread.
@@ -56,7 +56,8 @@ pm_status cuda_status(cudaError_t e) { return e == cudaSuccess ? PM_OK : PM_ERR_
 pm_status adf_impl(const float* in, float* out, int32_t W, int32_t H, int32_t B, const pm_intrinsics* K,
                    float lam, float kappa, int32_t iters, float* normals, void* ws, size_t ws_bytes,
                    int32_t iters_per_pass, int32_t scheme, int32_t nmode, int32_t engine, cudaStream_t stream) {
-    if (engine != PM_ADF_ENGINE_AUTO && engine != PM_ADF_ENGINE_TILED && engine != PM_ADF_ENGINE_REG)
+    if (engine != PM_ADF_ENGINE_AUTO && engine != PM_ADF_ENGINE_TILED && engine != PM_ADF_ENGINE_REG &&
+        engine != PM_ADF_ENGINE_HOLES)
         return PM_ERR_INVALID_ARGUMENT;
     if (scheme != PM_ADF_ALG1 && scheme != PM_ADF_DIVERGENCE) return PM_ERR_INVALID_ARGUMENT;
     if (nmode != PM_NORMALS_GEOMETRIC && nmode != PM_NORMALS_AS_PRINTED) return PM_ERR_INVALID_ARGUMENT;
@@ -136,7 +137,7 @@ extern "C" {
 
 PM_API size_t pm_adf_workspace_bytes(int32_t W, int32_t H, int32_t n_frames) {
     if (W < 1 || H < 1 || n_frames < 1) return 0;
-    return pm::adf_flags_offset(W, H, n_frames) + ((sizeof(int) * (size_t)n_frames + 255) & ~(size_t)255);
+    return pm::adf_flags_offset(W, H, n_frames) + pm::adf_flags_region_bytes(W, H, n_frames);
 }
 
 PM_API pm_status pm_adf_filter(const float* depth_in, float* depth_out, int32_t W, int32_t H,

@@ -13,6 +13,7 @@ cudaError_t adf_setup_attributes();
 int adf_default_iters_per_pass();
 // byte offset of the per-frame validity flags inside the adf workspace
 size_t adf_flags_offset(int W, int H, int B);
+size_t adf_flags_region_bytes(int W, int H, int B);   // frame flags + per-tile hole lists
 // lambda bound under which a frame whose ADF flag is 0 (every input depth
 // valid and in [2^-100, 2^100), adf.cu fast_depth) filters to valid depths only
 constexpr float kNoCheckMaxLambda = 0.249f;

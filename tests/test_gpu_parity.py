@@ -668,7 +668,9 @@ REG_FRAMES = [("C2", {}), ("C2", {"holes": 0.01}), ("C2", {"W": 332, "H": 251}),
 def test_reg_engine_bitwise_equals_tiled(pm, name, kw):
     """The register engine evaluates the identical per-cell expression, so it
     must equal the shared-memory engine bit for bit: every T, both schemes,
-    both normal modes, lambda at the stability limit (validity carried)."""
+    both normal modes, lambda at the stability limit (validity carried).  So
+    must the HOLES engine (unchecked walk + fix-up of the cells next to a
+    hole, hole lists carried from the first pass)."""
     fr = scenegen.make_config(name, **kw)
     d = fr["depth"].to(DEV)
     it = 9
@@ -679,10 +681,11 @@ def test_reg_engine_bitwise_equals_tiled(pm, name, kw):
         ref, nref = pm.adf_filter(d, fr["K"], lam, fr["kappa"], it, scheme=scheme, normals_mode=nmode,
                                   engine=pm.ENGINE_TILED)
         for T in (1, 2, 3, 4, 5, 7, 9):
-            out, nrm = pm.adf_filter(d, fr["K"], lam, fr["kappa"], it, scheme=scheme, normals_mode=nmode,
-                                     engine=pm.ENGINE_REG, iters_per_pass=T)
-            assert torch.equal(out, ref), (scheme, nmode, lam, T)
-            assert torch.equal(nrm, nref), (scheme, nmode, lam, T)
+            for eng in (pm.ENGINE_REG, pm.ENGINE_HOLES):
+                out, nrm = pm.adf_filter(d, fr["K"], lam, fr["kappa"], it, scheme=scheme, normals_mode=nmode,
+                                         engine=eng, iters_per_pass=T)
+                assert torch.equal(out, ref), (scheme, nmode, lam, T, eng)
+                assert torch.equal(nrm, nref), (scheme, nmode, lam, T, eng)
     # standalone normals (0 sweeps) and N = 0
     n_reg = pm.normals_from_depth(d, fr["K"])
     out0, n0 = pm.adf_filter(d, fr["K"], fr["lam"], fr["kappa"], 0, engine=pm.ENGINE_REG)
@@ -702,6 +705,22 @@ def test_reg_engine_batched_stream_equals_tiled(pm):
     ref, nref = pm.adf_filter(d, K, 0.15, 0.03, 20, engine=pm.ENGINE_TILED)
     out, nrm = pm.adf_filter(d, K, 0.15, 0.03, 20)
     assert torch.equal(out, ref) and torch.equal(nrm, nref)
+
+
+@pytest.mark.parametrize("frac", [0.0005, 0.01, 0.02, 0.05])
+def test_holes_engine_dropout_stream_equals_tiled(pm, frac):
+    """PM_ADF_ENGINE_HOLES on C4-size frames with dropout (the fix-up path,
+    its per-tile hole lists reused by the later passes, and above ~1.5 % the
+    checked-walk fallback) against the tiled engine, bit for bit; the frame
+    flags it leaves let the pipeline's compaction skip nothing it must read."""
+    d, lab, K = scenegen.stair_stream(40, 6, 640, 480, 64, device=DEV)
+    for i in range(d.shape[0]):
+        d[i] = scenegen.dropout(d[i], frac, 77 + i, i)
+    d[1] = scenegen.stair_stream(46, 1, 640, 480, 64, device=DEV)[0][0]     # one hole-free frame in the batch
+    for T in (4, 3, 16):
+        ref, nref = pm.adf_filter(d, K, 0.15, 0.03, 20, engine=pm.ENGINE_TILED, iters_per_pass=T)
+        out, nrm = pm.adf_filter(d, K, 0.15, 0.03, 20, engine=pm.ENGINE_HOLES, iters_per_pass=T)
+        assert torch.equal(out, ref) and torch.equal(nrm.nan_to_num(7.0), nref.nan_to_num(7.0)), (frac, T)
 
 
 def test_binding_rejects_mismatched_buffers(pm):

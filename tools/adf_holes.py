@@ -1,5 +1,8 @@
 #!/usr/bin/env python
-"""ADF+normals stage on 512 C4 frames, hole-free and with 1 % dropout holes."""
+"""ADF+normals stage on 512 C4 frames: hole-free and with 0.1 / 1 / 3 / 6 %
+dropout holes, the default (TILED) engine and PM_ADF_ENGINE_HOLES; each
+result compared bit for bit with the register engine (an independent
+hole-aware walk)."""
 import os
 import sys
 
@@ -12,15 +15,16 @@ import scenegen
 B = 512
 dev = torch.device("cuda", 0)
 d, lab, K = scenegen.stair_stream(0, B, 640, 480, 64, device=dev)
-dh = d.clone()
-for i in range(B):
-    dh[i] = scenegen.dropout(dh[i], 0.01, 1000 + i, i)
 out = torch.empty_like(d)
 nrm = torch.empty(B, 3, 480, 640, device=dev)
 ws = torch.empty(pm.adf_workspace_bytes(640, 480, B), dtype=torch.uint8, device=dev)
 res = {}
-for name, x in (("hole-free", d), ("1% holes", dh)):
-    f = lambda: pm.adf_filter(x, K, 0.15, 0.03, 20, out=out, normals_out=nrm, workspace=ws)
+for frac, eng in [(f, e) for f in (0.0, 0.001, 0.01, 0.03, 0.06) for e in (pm.ENGINE_TILED, pm.ENGINE_HOLES)]:
+    x = d.clone()
+    if frac:
+        for i in range(B):
+            x[i] = scenegen.dropout(x[i], frac, 1000 + i, i)
+    f = lambda: pm.adf_filter(x, K, 0.15, 0.03, 20, out=out, normals_out=nrm, workspace=ws, engine=eng)
     for _ in range(3):
         f()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -30,6 +34,10 @@ for name, x in (("hole-free", d), ("1% holes", dh)):
         f()
     e1.record()
     torch.cuda.synchronize()
-    res[name] = e0.elapsed_time(e1) / 10
-    print(f"{name:10s}: {res[name]:.3f} ms per 512 frames")
-print(f"ratio holes / hole-free: {res['1% holes'] / res['hole-free']:.2f}")
+    res[frac, eng] = e0.elapsed_time(e1) / 10
+    ro, rn = pm.adf_filter(x[:32], K, 0.15, 0.03, 20, engine=pm.ENGINE_REG)
+    same = torch.equal(out[:32], ro) and torch.equal(nrm[:32].nan_to_num(7.0), rn.nan_to_num(7.0))
+    name = "holes" if eng == pm.ENGINE_HOLES else "tiled"
+    print(f"{100 * frac:4.1f} % holes, {name}: {res[frac, eng]:.3f} ms per 512 frames  "
+          f"({res[frac, eng] / res[0.0, pm.ENGINE_TILED]:.2f}x hole-free tiled)"
+          f"  bitwise = register engine: {same}")

@@ -15,12 +15,12 @@ import scenegen
 
 fr = scenegen.make_config("C1n", holes=0.02)
 d, lab, K = fr["depth"].cuda(), fr["labels"].cuda(), fr["K"]
-for eng in (pm.ENGINE_TILED, pm.ENGINE_REG):
+for eng in (pm.ENGINE_TILED, pm.ENGINE_REG, pm.ENGINE_HOLES):
     for scheme in (pm.ADF_ALG1, pm.ADF_DIVERGENCE):
         out, nrm = pm.adf_filter(d, K, 0.15, 0.03, 10, engine=eng, scheme=scheme)
 fr2 = scenegen.make_config("C2", W=256, H=160, holes=0.01)
 d2 = fr2["depth"].cuda()
-for eng in (pm.ENGINE_TILED, pm.ENGINE_REG):
+for eng in (pm.ENGINE_TILED, pm.ENGINE_REG, pm.ENGINE_HOLES):
     for lam in (0.15, 0.25):
         pm.adf_filter(d2, fr2["K"], lam, 0.03, 9, engine=eng, iters_per_pass=4)
         pm.adf_filter(d2, fr2["K"], lam, 0.03, 9, engine=eng, iters_per_pass=3, normals_mode=pm.NORMALS_AS_PRINTED)
