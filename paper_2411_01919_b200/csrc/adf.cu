@@ -256,8 +256,17 @@ adf_pass_kernel(const float* __restrict__ src, float* __restrict__ dst, float* _
             mbar_arrive_expect_tx(&bar, (uint32_t)(sizeof(float) * kSW * SH));
             tma_load_3d(buf0, &tmap, x0, y0, (int)frame, &bar);
         }
+        // FIX, list_mode 2: the frame flag and this tile's hole-list record
+        // fetched while the tile streams in (the record speculatively)
+        int lflag = 1;                          // the frame flag (flag_mode 2), fetched while the tile streams in
+        uint4 lrec = make_uint4(0u, 0u, 0u, 0u);
+        if (flag_mode == 2) lflag = frame_flags[frame];
+        if (FIX && flag_mode == 2 && list_mode == 2 && threadIdx.x <= kListVecs)
+            lrec = tile_lists[tile_index() * (kListVecs + 1) + threadIdx.x];   // (speculative)
         mbar_wait(&bar, 0);
 #else
+        const int lflag = flag_mode == 2 ? frame_flags[frame] : 1;
+        uint4 lrec = make_uint4(0u, 0u, 0u, 0u);
         for (int i = threadIdx.x; i < kSW * SH; i += kThreads) buf0[i] = 1.0f + 1e-3f * (i & 7);
         __syncthreads();
 #endif
@@ -266,8 +275,8 @@ adf_pass_kernel(const float* __restrict__ src, float* __restrict__ dst, float* _
         // Passes with the first pass's tile geometry read that pass's hole
         // lists instead (list_mode 2; loads overlap the tile load).
         if (FIX && flag_mode == 2 && list_mode == 2) {
-            if (frame_flags[frame] != 0 && threadIdx.x <= kListVecs) {
-                const uint4 v = tile_lists[tile_index() * (kListVecs + 1) + threadIdx.x];
+            if (lflag != 0 && threadIdx.x <= kListVecs) {
+                const uint4 v = lrec;
                 if (threadIdx.x == 0) {
                     const uint32_t c[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
@@ -278,7 +287,7 @@ adf_pass_kernel(const float* __restrict__ src, float* __restrict__ dst, float* _
             } else if (threadIdx.x < kWarps) {
                 s_wn[threadIdx.x] = 0;
             }
-        } else if (flag_mode != 2 || frame_flags[frame] != 0) {
+        } else if (lflag != 0) {
             const int c0 = 4 * lane;  // (4 columns per lane: 32 lanes cover the 128-column tile)
             bool in[4];
 #pragma unroll
@@ -369,11 +378,13 @@ adf_pass_kernel(const float* __restrict__ src, float* __restrict__ dst, float* _
         item[r] = -1;
         const int k = threadIdx.x + r * kThreads;
         if (fixup && k < 5 * nh) {
-            int h = k / 5;
+            const int h = k / 5;
             const int d = k - 5 * h;
-            int w = 0;
-            while (h >= s_wn[w]) h -= s_wn[w++];
-            const int e = hl[w * kWarpHoles + h];
+            int slot = h;                              // the h-th hole of the flattened lists
+#pragma unroll
+            for (int w = 1; w < kWarps; ++w)
+                if (h >= pre[w]) slot = h - pre[w] + w * kWarpHoles;
+            const int e = hl[slot];
             item[r] = e + (d == 1 ? -kSW : d == 2 ? kSW : d == 3 ? -1 : d == 4 ? 1 : 0);
             if ((d == 3 && (e & 127) == 0) || (d == 4 && (e & 127) == kSW - 1)) item[r] = -1;
         }
@@ -412,12 +423,13 @@ adf_pass_kernel(const float* __restrict__ src, float* __restrict__ dst, float* _
     };
     bool done = false;
     if constexpr (R <= 6) {
-        if (fast && b.ix0 == 0 && b.ix1 == kSW && b.iy0 == 0 && b.iy1 == SH) {
+        if ((fast || fixup) && b.ix0 == 0 && b.ix1 == kSW && b.iy0 == 0 && b.iy1 == SH) {
             constexpr Box kIn{0, kSW, 0, SH};
 #pragma unroll
             for (int t = 1; t <= R; ++t) {
                 if (t > iters) break;
                 sweep_pairs<SH, PAD, false, DIV>(cur, nxt, t, kIn, p);
+                if (FIX && fixup) fix(t);
                 __syncthreads();
                 float* tmp = cur; cur = nxt; nxt = tmp;
             }
