@@ -467,6 +467,24 @@ adf_pass_kernel(const float* __restrict__ src, float* __restrict__ dst, float* _
     const int ox = blockIdx.x * TW, oy = blockIdx.y * kTH;
     float* out = dst ? dst + frame * HW : nullptr;
     float* nrm = normals ? normals + frame * 3 * HW : nullptr;
+#ifndef PM_ADF_QUAD_STORES
+    // plain passes: each output row leaves shared memory as one bulk copy
+    // (cp.async.bulk), issued by one thread per row -- the tile's stores
+    // cost 44 instructions instead of a load / store pair per float4
+    if (!nrm && out && (W & 3) == 0 && ((uintptr_t)out & 15) == 0) {
+        const int y = threadIdx.x, gy = oy + y;
+        if (y < kTH && gy < H) {
+            const int w = min(TW, W - ox);
+            fence_proxy_async_smem();             // the last sweep's stores, before the async proxy reads
+            bulk_store_s2g(out + (size_t)gy * W + ox, cur + (y + R) * kSW + RA, (uint32_t)(sizeof(float) * w));
+            bulk_commit();
+            bulk_wait_read();
+        }
+        PM_ATS(t3);
+        PM_AACC(pk_ + 2, t2, t3);
+        return;
+    }
+#endif
     if ((W & 3) == 0) {
         constexpr int QW = TW / 4;
         // CK: window validity checks (tiles with holes); NMC: normals mode

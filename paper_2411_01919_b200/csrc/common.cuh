@@ -135,6 +135,17 @@ PM_DEVINL void mbar_wait(uint64_t* bar, uint32_t parity) {
         : "memory");
 }
 
+// Bulk copy shared -> global (cp.async.bulk, bulk-group completion): 16-B
+// aligned addresses, size a multiple of 16.  Pair with bulk_commit() and
+// bulk_wait_read() (the source may be overwritten / the CTA exit after it).
+PM_DEVINL void bulk_store_s2g(void* dst, const void* src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"((uint64_t)dst),
+                 "r"(smem_u32(src)), "r"(bytes)
+                 : "memory");
+}
+PM_DEVINL void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+PM_DEVINL void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+
 // 3-D tile load global -> shared, completion signalled on `bar` (tx bytes).
 PM_DEVINL void tma_load_3d(void* dst, const CUtensorMap* map, int x, int y, int z, uint64_t* bar) {
     asm volatile(
