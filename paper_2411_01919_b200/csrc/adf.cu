@@ -292,6 +292,7 @@ adf_pass_kernel(const float* __restrict__ src, float* __restrict__ dst, float* _
             bool in[4];
 #pragma unroll
             for (int j = 0; j < 4; ++j) in[j] = c0 + j >= b.ix0 && c0 + j < b.ix1;
+#pragma unroll(FIX ? 1 : (SH + kWarps - 1) / kWarps)
             for (int sy = b.iy0 + warp; sy < b.iy1; sy += kWarps) {
                 const float4 v = *reinterpret_cast<const float4*>(buf0 + sy * kSW + c0);
                 if constexpr (!FIX) {
