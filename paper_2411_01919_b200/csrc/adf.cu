@@ -95,6 +95,8 @@ PM_DEVINL void sweep(const float* __restrict__ cur, float* __restrict__ nxt, int
         const float S = col[(y + 1) * kSW];
         const float W = colW[y * kSW];
         const float E = colE[y * kSW];
+        PM_CHECK(ocol + y * kSW - nxt >= 0 && ocol + y * kSW - nxt < kSW * SH);
+        PM_CHECK(col + (y + 1) * kSW - cur < kSW * (SH + 1) && colW + y * kSW - cur >= 0);
         ocol[y * kSW] = cell<CHECK, DIV>(C, N, S, W, E, p);
         N = C;
         C = S;
@@ -159,6 +161,8 @@ PM_DEVINL void sweep_pairs(const float* __restrict__ cur, float* __restrict__ nx
     float2 S = ld2(col + kSW);
     float2 P = make_float2(colW[0], colE[0]);
     auto step = [&]() {
+        PM_CHECK(col + 2 * kSW - cur + 2 <= kSW * (SH + 1) && colW + kSW - cur >= 0 && colE + kSW - cur < kSW * (SH + 1));
+        PM_CHECK(ocol - nxt >= 0 && ocol - nxt + 2 <= kSW * SH);
         const float2 S1 = ld2(col + 2 * kSW);
         const float2 P1 = make_float2(colW[kSW], colE[kSW]);
         *reinterpret_cast<float2*>(ocol) = cellp(C, N, S, P);
@@ -385,6 +389,7 @@ adf_pass_kernel(const float* __restrict__ src, float* __restrict__ dst, float* _
 #pragma unroll
             for (int w = 1; w < kWarps; ++w)
                 if (h >= pre[w]) slot = h - pre[w] + w * kWarpHoles;
+            PM_CHECK(slot >= 0 && slot < kWarps * kWarpHoles);
             const int e = hl[slot];
             item[r] = e + (d == 1 ? -kSW : d == 2 ? kSW : d == 3 ? -1 : d == 4 ? 1 : 0);
             if ((d == 3 && (e & 127) == 0) || (d == 4 && (e & 127) == kSW - 1)) item[r] = -1;
@@ -413,6 +418,7 @@ adf_pass_kernel(const float* __restrict__ src, float* __restrict__ dst, float* _
             const int e = item[r];
             const int sy = e >> 7, sx = e & 127;
             if (e < 0 || sy < ylo || sy >= yhi || sx < xlo || sx >= xhi) continue;
+            PM_CHECK(e - kSW >= 0 && e + kSW < kSW * SH && sx >= 1 && sx + 1 < kSW);
             const float* c = cur + e;
             const float C = c[0];
             const float N = sy == b.iy0 ? C : c[-kSW];
@@ -476,6 +482,7 @@ adf_pass_kernel(const float* __restrict__ src, float* __restrict__ dst, float* _
         const int y = threadIdx.x, gy = oy + y;
         if (y < kTH && gy < H) {
             const int w = min(TW, W - ox);
+            PM_CHECK(w > 0 && ox + w <= W && y + R < SH && RA + w <= kSW && ((w * 4) & 15) == 0);
             fence_proxy_async_smem();             // the last sweep's stores, before the async proxy reads
             bulk_store_s2g(out + (size_t)gy * W + ox, cur + (y + R) * kSW + RA, (uint32_t)(sizeof(float) * w));
             bulk_commit();

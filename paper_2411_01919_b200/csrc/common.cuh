@@ -9,6 +9,21 @@
 
 #define PM_DEVINL __device__ __forceinline__
 
+// Checked build (compute-sanitizer substitute, tools/checked_run.sh): device
+// bounds checks on the shared- and global-memory indices of the hot kernels;
+// a failed check traps (the launch then fails with an illegal-instruction
+// error).  Empty in the product build.
+#ifdef PM_CHECKED
+#define PM_CHECK(cond)               \
+    do {                             \
+        if (!(cond)) __trap();       \
+    } while (0)
+#else
+#define PM_CHECK(cond) \
+    do {               \
+    } while (0)
+#endif
+
 namespace pm {
 
 constexpr int kWarp = 32;

@@ -272,12 +272,14 @@ compact_scatter_kernel(const float* __restrict__ depth, const int32_t* __restric
                         b = off[lab] + r0;
                     }
                     b = __shfl_sync(kFull, b, leader);
+                    PM_CHECK(lab < 0 || (b + __popc(m & lt) >= 0 && b + __popc(m & lt) < WH));
                     if (lab >= 0) pts[b + __popc(m & lt)] = pk;
                     __syncwarp();
                 }
             }
             if (fast) {
                 const unsigned bal = __ballot_sync(kFull, lab >= 0);
+                PM_CHECK(lab < 0 || (roff + rel + __popc(bal & lt) >= 0 && roff + rel + __popc(bal & lt) < WH));
                 if (lab >= 0) pts[roff + rel + __popc(bal & lt)] = pk;
                 rel += __popc(bal);
             }

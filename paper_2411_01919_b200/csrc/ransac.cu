@@ -119,6 +119,7 @@ ransac_hyp_kernel(RansacWorkspace ws, RansacArgs a, int need_err) {
         if (s.ok) {
             const uint2* pts = ws.points + f * (size_t)ws.W * ws.H + off[r];
             const float ifx = 1.0f / a.K.fx, ify = 1.0f / a.K.fy;   // host-identical IEEE division
+            PM_CHECK(s.i0 < n && s.i1 < n && s.i2 < n && off[r] + n <= ws.W * ws.H);
             const uint2 q0 = pts[s.i0], q1 = pts[s.i1], q2 = pts[s.i2];
             const float3 p0 = deproject(PackedPoint{q0.x, __uint_as_float(q0.y)}, a.K.cx, a.K.cy, ifx, ify);
             const float3 p1 = deproject(PackedPoint{q1.x, __uint_as_float(q1.y)}, a.K.cx, a.K.cy, ifx, ify);
@@ -176,6 +177,7 @@ PM_DEVINL bool stage_chunk(const RansacWorkspace& ws, const RansacArgs& a, size_
     const uint2* pts = ws.points + f * (size_t)ws.W * ws.H;
     const float ifx = 1.0f / a.K.fx, ify = 1.0f / a.K.fy;   // IEEE division, as on the host
     for (int i = threadIdx.x; i < ck.e - ck.s; i += kScoreThreads) {
+        PM_CHECK(i < kScoreChunk && ck.s + i < ws.W * ws.H);
         const uint2 q = pts[ck.s + i];
         const float3 P = deproject(PackedPoint{q.x, __uint_as_float(q.y)}, a.K.cx, a.K.cy, ifx, ify);
         sp[i] = make_float4(P.x, P.y, P.z, 0.f);
@@ -540,6 +542,7 @@ ransac_refit_kernel(RansacWorkspace ws, RansacArgs a) {
                     const uint2* sp = (half ? sb1 + sh1 - hs1 : sb0 + sh0 - hs0);
 #pragma unroll 4
                     for (int i = b0 + lane; i < b1; i += 32) {
+                        PM_CHECK(&sp[i] >= s_pts && &sp[i] < s_pts + kRefitWarps * 2 * kHalfSlot);
                         const uint2 q = sp[i];
                         const float3 P = deproject(PackedPoint{q.x, __uint_as_float(q.y)}, a.K.cx, a.K.cy, ifx, ify);
                         const float dist = plane_dist(pl, P);
@@ -560,6 +563,7 @@ ransac_refit_kernel(RansacWorkspace ws, RansacArgs a) {
             // one slot per (chunk + region, warp), zero when the warp's span
             // misses the region: no block barrier; the finalize kernel sums
             // them in (chunk, warp) order (deterministic)
+            PM_CHECK(blockIdx.x + r < ws.n_slots);
             if (lane == 0) ws.slots[(f * (size_t)ws.n_slots + blockIdx.x + r) * kRefitWarps + w] = acc;
         }
     }
