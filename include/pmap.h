@@ -117,7 +117,10 @@ PM_API size_t pm_adf_workspace_bytes(int32_t W, int32_t H, int32_t n_frames);
  *   PM_NORMALS_AS_PRINTED  Eq. 2 literally: n = -K^-1 [Gx, Gy, 1]^T, normalised */
 enum { PM_ADF_ALG1 = 0, PM_ADF_DIVERGENCE = 1 };
 enum { PM_NORMALS_GEOMETRIC = 0, PM_NORMALS_AS_PRINTED = 1 };
-/* engine: AUTO = TILED (the faster engine on B200);
+/* engine: AUTO = TILED (the faster engine on B200), switching
+ * to HOLES while a call on the device within the last 16 multi-pass calls met
+ * an invalid pixel (the first pass notes it in a mapped host word; results
+ * are the same either way);
  * REG = register-resident tiles (csrc/adf_reg.cu; W % 4 == 0, H >= 128,
  * 16-B aligned depth), falls back to TILED where it does not apply;
  * TILED = shared-memory tiles, iters_per_pass sweeps (default 4) per HBM pass;

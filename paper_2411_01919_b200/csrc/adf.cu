@@ -28,6 +28,8 @@
 #include <stdint.h>
 #include <string.h>
 
+#include <atomic>
+#include <mutex>
 #include <type_traits>
 
 #include "adf_cell.cuh"
@@ -341,7 +343,10 @@ adf_pass_kernel(const float* __restrict__ src, float* __restrict__ dst, float* _
         if (lane == 0 && !(flag_mode == 2 && list_mode == 2)) s_wn[warp] = wn;
     }
     all_valid = __syncthreads_and(all_valid);
-    if (flag_mode == 1 && !all_valid && threadIdx.x == 0) atomicOr(frame_flags + frame, 1);
+    if (flag_mode == 1 && !all_valid && threadIdx.x == 0) {
+        atomicOr(frame_flags + frame, 1);
+        if (p.hole_note) *(volatile unsigned*)p.hole_note = p.call_id;
+    }
     // tiles with a few holes: the unchecked walk everywhere, then the cells
     // whose stencil touches a listed cell (the cell itself and its 4
     // neighbours) recomputed with the checked cell -- every other cell's
@@ -672,13 +677,60 @@ static AdfParams make_params(const pm_intrinsics* K, float lam, float kappa, int
     p.scheme = scheme;
     p.nmode = nmode;
     p.keep_valid = lam > kNoCheckMaxLambda ? 1 : 0;
+    p.hole_note = nullptr;
+    p.call_id = 0;
     return p;
 }
+
+// AUTO engine choice: the hole engine (FIX kernels) while a recent call on
+// this device saw an invalid pixel, the lean tiled kernels otherwise.  The
+// first pass of a multi-pass call stores the call's id into a mapped host
+// word when one of its tiles holds an invalid pixel (the frame-flag branch);
+// the host reads it when the next call is made -- no copy, no stream
+// operation.  Results do not depend on the choice (the engines are bitwise
+// equal); only the speed on frames with dropout does.
+namespace {
+constexpr unsigned kHoleMemory = 16;   // calls a hole observation keeps AUTO on the hole engine
+struct HoleNote {
+    std::once_flag once;
+    unsigned* host = nullptr;          // mapped pinned word (host view)
+    unsigned* dev = nullptr;           // its device view
+    std::atomic<unsigned> calls{0};
+};
+HoleNote g_hole_note[64];
+HoleNote* hole_note(cudaStream_t stream) {
+    int d = 0;
+    if (cudaGetDevice(&d) != cudaSuccess || d < 0 || d >= 64) return nullptr;
+    HoleNote& n = g_hole_note[d];
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(stream, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) {
+        (void)cudaGetLastError();
+        return n.host ? &n : nullptr;  // (no allocation inside a graph capture)
+    }
+    std::call_once(n.once, [&] {
+        unsigned* h = nullptr;
+        unsigned* dp = nullptr;
+        if (cudaHostAlloc(&h, sizeof(unsigned), cudaHostAllocMapped) != cudaSuccess) {
+            (void)cudaGetLastError();
+            return;
+        }
+        *h = 0;
+        if (cudaHostGetDevicePointer(&dp, h, 0) != cudaSuccess) {
+            (void)cudaGetLastError();
+            cudaFreeHost(h);
+            return;
+        }
+        n.dev = dp;
+        n.host = h;
+    });
+    return n.host ? &n : nullptr;
+}
+}  // namespace
 
 cudaError_t adf_run(const float* in, float* out, float* normals, float* ws, int W, int H, int B,
                     const pm_intrinsics* K, float lam, float kappa, int iters, int iters_per_pass,
                     int scheme, int nmode, int engine, cudaStream_t stream) {
-    const AdfParams p = make_params(K, lam, kappa, scheme, nmode);
+    AdfParams p = make_params(K, lam, kappa, scheme, nmode);
     int T = iters_per_pass > 0 ? iters_per_pass : adf_default_iters_per_pass();
     if (T > kMaxItersPerPass) T = kMaxItersPerPass;
     if (iters == 0) {   // N = 0: I_smooth = I (Alg. 1 ℓ1); normals of the input
@@ -703,7 +755,16 @@ cudaError_t adf_run(const float* in, float* out, float* normals, float* ws, int 
     int done = 0;
     // the register engine is opt-in: measured slower than the tiled engine on B200
     const bool try_reg = engine == PM_ADF_ENGINE_REG;
-    const bool fix = engine == PM_ADF_ENGINE_HOLES;   // the tiled engine with the fix-up walk
+    bool fix = engine == PM_ADF_ENGINE_HOLES;         // the tiled engine with the fix-up walk
+    if (flags && (engine == PM_ADF_ENGINE_AUTO || engine == PM_ADF_ENGINE_HOLES)) {
+        if (HoleNote* n = hole_note(stream)) {
+            const unsigned id = n->calls.fetch_add(1) + 1u;
+            const unsigned seen = *(volatile unsigned*)n->host;
+            if (engine == PM_ADF_ENGINE_AUTO && seen != 0 && id - seen <= kHoleMemory) fix = true;
+            p.hole_note = n->dev;
+            p.call_id = id;
+        }
+    }
     bool lists_written = false;   // by a tiled first pass
     for (int k = 0; k < passes; ++k) {
         const int it = (iters - done) / (passes - k);   // near-equal split, sums to iters

@@ -25,6 +25,8 @@ struct AdfParams {
     int nmode;        // PM_NORMALS_GEOMETRIC | PM_NORMALS_AS_PRINTED
     int keep_valid;   // lambda > kNoCheckMaxLambda: floor valid updates at the
                       // smallest positive float (see keep_valid() below)
+    unsigned* hole_note;   // mapped host word: the first pass stores call_id on a tile with
+    unsigned call_id;      // an invalid pixel (AUTO engine choice, adf.cu), or null
 };
 
 // Q4 fixes validity from the INPUT of the filter.  For lambda <= 0.249 no
