@@ -358,8 +358,10 @@ def extra_configs(pm, dev, clk_mhz, hbm_peak):
     torch.cuda.synchronize()
     res["C4_holes_1pct"] = {"value": B / (ms / 1e3), "unit": "frames/s", "frames_per_step": B, "ms_per_step": ms,
                             "stages_ms": st, "adf_normals_ms_engine_holes": e0.elapsed_time(e1) / 5,
-                            "workload": "C4 stream with 1 % hash-selected dropout holes per frame (default engine; "
-                                        "adf_normals_ms_engine_holes: the ADF stage with PM_ADF_ENGINE_HOLES)"}
+                            "workload": "C4 stream with 1 % hash-selected dropout holes per frame (the default "
+                                        "AUTO engine, which runs the hole engine while recent calls met invalid "
+                                        "pixels; adf_normals_ms_engine_holes: the ADF stage with "
+                                        "PM_ADF_ENGINE_HOLES explicitly)"}
     del d, lab, bb
     torch.cuda.empty_cache()
 
