@@ -776,6 +776,9 @@ cudaError_t adf_run(const float* in, float* out, float* normals, float* ws, int 
         const int it0 = iters / passes;
         const bool fused = last && normals != nullptr;
         int lmode = !flags || !fix ? 0 : k == 0 ? (fused ? 0 : 1) : (!fused && it == it0 && lists_written ? 2 : 0);
+#ifdef PM_ADF_EXP_NOLISTS
+        lmode = 0;
+#endif
         uint4* lists = flags ? reinterpret_cast<uint4*>(reinterpret_cast<char*>(flags) + adf_lists_offset(B)) : nullptr;
         bool launched = false;
         if (try_reg) {
