@@ -56,6 +56,7 @@ pm_status cuda_status(cudaError_t e) { return e == cudaSuccess ? PM_OK : PM_ERR_
 pm_status adf_impl(const float* in, float* out, int32_t W, int32_t H, int32_t B, const pm_intrinsics* K,
                    float lam, float kappa, int32_t iters, float* normals, void* ws, size_t ws_bytes,
                    int32_t iters_per_pass, int32_t scheme, int32_t nmode, int32_t engine, cudaStream_t stream) {
+    const pm::NvtxRange nvtx_("pmap:adf_filter");
     if (engine != PM_ADF_ENGINE_AUTO && engine != PM_ADF_ENGINE_TILED && engine != PM_ADF_ENGINE_REG &&
         engine != PM_ADF_ENGINE_HOLES)
         return PM_ERR_INVALID_ARGUMENT;
@@ -83,6 +84,7 @@ pm_status ransac_impl(const float* depth, int32_t W, int32_t H, int32_t B, uint3
                       const pm_intrinsics* K, const int32_t* labels, int32_t R, int32_t n_hyp,
                       float tau, uint64_t seed, pm_plane* planes, void* ws, size_t ws_bytes,
                       const pm_ransac_options* opt, cudaStream_t stream, const int* depth_all_valid = nullptr) {
+    const pm::NvtxRange nvtx_("pmap:ransac_planes");
     if (!depth || !labels || !dims_ok(W, H, B) || !intrinsics_ok(K)) return PM_ERR_INVALID_ARGUMENT;
     if (R < 0 || R > 65536 || n_hyp < 1 || n_hyp > 4096 || !finite_pos(tau)) return PM_ERR_INVALID_ARGUMENT;
     if (R > 0 && !planes) return PM_ERR_INVALID_ARGUMENT;
@@ -179,6 +181,7 @@ PM_API pm_status pm_normals_from_depth_batched(const float* depth, int32_t W, in
 PM_API pm_status pm_normals_from_depth_ex(const float* depth, int32_t W, int32_t H, int32_t n_frames,
                                           const pm_intrinsics* K, int32_t mode, float* normals_out,
                                           pm_stream_t stream) {
+    const pm::NvtxRange nvtx_("pmap:normals_from_depth");
     if (!depth || !normals_out || !dims_ok(W, H, n_frames) || !intrinsics_ok(K)) return PM_ERR_INVALID_ARGUMENT;
     if (mode != PM_NORMALS_GEOMETRIC && mode != PM_NORMALS_AS_PRINTED) return PM_ERR_INVALID_ARGUMENT;
     const size_t bytes = sizeof(float) * (size_t)n_frames * W * H;
@@ -231,6 +234,7 @@ PM_API pm_status pm_process_frames(const float* depth_in, const int32_t* region_
                                    float lambda, float kappa, int32_t iters, int32_t n_regions, int32_t n_hyp,
                                    float inlier_thresh, uint64_t seed, float* depth_out, float* normals_out,
                                    pm_plane* planes_out, void* workspace, size_t ws_bytes, pm_stream_t stream) {
+    const pm::NvtxRange nvtx_("pmap:process_frames");
     if (!depth_out || !normals_out) return PM_ERR_INVALID_ARGUMENT;
     if (ws_bytes < pm_pipeline_workspace_bytes(W, H, n_regions, n_hyp, n_frames)) return PM_ERR_WORKSPACE;
     pm_status s = adf_impl(depth_in, depth_out, W, H, n_frames, K, lambda, kappa, iters, normals_out, workspace,

@@ -187,6 +187,7 @@ pm_status host_pipeline(const void* depth_host, int32_t depth_format, const void
                         float inlier_thresh, uint64_t seed, pm_plane* planes_host, float* depth_out_host,
                         float* normals_host, int32_t chunk_frames, void* arena, size_t arena_bytes,
                         pm_stream_t stream, bool async) {
+    const pm::NvtxRange nvtx_("pmap:process_frames_host");
     if (!depth_host || !labels_host || !planes_host || chunk_frames < 1 || n_frames < 1)
         return PM_ERR_INVALID_ARGUMENT;
     if (depth_format != PM_DEPTH_F32_M && depth_format != PM_DEPTH_U16_MM) return PM_ERR_INVALID_ARGUMENT;

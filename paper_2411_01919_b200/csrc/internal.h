@@ -6,7 +6,18 @@
 
 #include "../../include/pmap.h"
 
+#include <nvtx3/nvToolsExt.h>
+
 namespace pm {
+
+// NVTX range around a C-ABI call (header-only NVTX v3: a no-op unless a tool
+// such as nsys / ncu injects itself), so host timelines show the pmap calls.
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 // ---- adf.cu
 cudaError_t adf_setup_attributes();

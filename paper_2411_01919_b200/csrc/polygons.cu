@@ -294,6 +294,7 @@ PM_API size_t pm_region_polygons_workspace_bytes(int32_t n_frames, int32_t n_reg
 PM_API pm_status pm_region_polygons(const int32_t* labels, int32_t W, int32_t H, int32_t n_frames, int32_t n_regions,
                                     const pm_polygon_params* prm, int32_t* contour_len, int32_t* vertices,
                                     int32_t* n_vertices, void* workspace, size_t ws_bytes, pm_stream_t stream) {
+    const pm::NvtxRange nvtx_("pmap:region_polygons");
     using namespace pm;
     if (!labels || !contour_len || !vertices || !n_vertices || W < 1 || H < 1 || W > 65535 || H > 65535 ||
         n_frames < 1 || n_regions < 0 || !params_ok(prm))
@@ -320,6 +321,7 @@ PM_API pm_status pm_region_polygons(const int32_t* labels, int32_t W, int32_t H,
 PM_API pm_status pm_rasterize_polygons(const int32_t* vertices, const int32_t* n_vertices, int32_t max_vertices,
                                        int32_t W, int32_t H, int32_t n_frames, int32_t n_regions, int32_t* labels_out,
                                        void* workspace, size_t ws_bytes, pm_stream_t stream) {
+    const pm::NvtxRange nvtx_("pmap:rasterize_polygons");
     using namespace pm;
     if (!vertices || !n_vertices || !labels_out || W < 1 || H < 1 || W > 65535 || H > 65535 || n_frames < 1 ||
         n_regions < 0 || max_vertices < 3)
@@ -339,6 +341,7 @@ PM_API pm_status pm_rasterize_polygons(const int32_t* vertices, const int32_t* n
 PM_API pm_status pm_lift_polygon_vertices(const int32_t* vertices, const int32_t* n_vertices, int32_t max_vertices,
                                           const pm_plane* planes, int32_t n_frames, int32_t n_regions,
                                           const pm_intrinsics* K, double* X_out, pm_stream_t stream) {
+    const pm::NvtxRange nvtx_("pmap:lift_polygon_vertices");
     using namespace pm;
     if (!vertices || !n_vertices || !planes || !X_out || !K || n_frames < 1 || n_regions < 0 || max_vertices < 3 ||
         !(K->fx > 0.0f) || !(K->fy > 0.0f))

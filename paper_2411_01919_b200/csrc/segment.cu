@@ -456,6 +456,7 @@ PM_API size_t pm_segment_workspace_bytes(int32_t W, int32_t H, int32_t n_frames,
 PM_API pm_status pm_segment_regions(const float* normals, int32_t W, int32_t H, int32_t n_frames,
                                     const pm_segment_params* prm, int32_t* labels_out, int32_t* n_regions_out,
                                     uint8_t* edges_out, void* workspace, size_t ws_bytes, pm_stream_t stream) {
+    const pm::NvtxRange nvtx_("pmap:segment_regions");
     using namespace pm;
     if (!normals || !labels_out || !prm || W < 3 || H < 3 || W > 65535 || H > 65535 || n_frames < 1 ||
         n_frames > 65535)
