@@ -197,7 +197,11 @@ PM_API size_t pm_ransac_workspace_bytes(int32_t W, int32_t H, int32_t n_regions,
 
 /* Test / paper-literal options for ransac (NEXT-1 rows of SURVEY §8(f)). */
 enum { PM_SAMPLER_PHILOX = 0, PM_SAMPLER_ENUMERATE = 1 };   /* ENUMERATE: h -> h-th 3-combination, colex */
-enum { PM_SELECT_COUNT = 0, PM_SELECT_ERROR = 1 };          /* ERROR: argmin Σd as printed       */
+enum { PM_SELECT_COUNT = 0, PM_SELECT_ERROR = 1,            /* ERROR: argmin Σd as printed       */
+       PM_SELECT_COUNT_EARLY = 2, PM_SELECT_ERROR_EARLY = 3 }; /* *_EARLY: the hypothesis loop stops once the
+                                                                  best model so far passes the 0.9 gate
+                                                                  ("until ... a satisfactory model is found",
+                                                                  P:292; Q20)                     */
 typedef struct {
     int32_t sampler;          /* PM_SAMPLER_*                                          */
     int32_t select;           /* PM_SELECT_*                                           */

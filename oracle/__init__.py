@@ -27,7 +27,7 @@ CFLAGS = ["-O2", "-std=c11", "-fPIC", "-shared", "-ffp-contract=off", "-fno-fast
 SAMPLER_PHILOX, SAMPLER_ENUMERATE = 0, 1
 ADF_ALG1, ADF_DIVERGENCE = 0, 1
 NORMALS_GEOMETRIC, NORMALS_AS_PRINTED = 0, 1
-SELECT_COUNT, SELECT_ERROR = 0, 1
+SELECT_COUNT, SELECT_ERROR, SELECT_COUNT_EARLY, SELECT_ERROR_EARLY = 0, 1, 2, 3
 STATUS_OK, STATUS_REJECTED, STATUS_TOO_FEW, STATUS_DEGENERATE = 0, 1, 2, 3
 
 

@@ -405,7 +405,11 @@ ORC_API int orc_refit_plane(const double* pts, int n, double out[7])
  *   errq_all[r*n_hyp + h] (nullable) fixed-point error per hypothesis        */
 enum { ORC_OK = 0, ORC_REJECTED = 1, ORC_TOO_FEW = 2, ORC_DEGENERATE = 3 };
 enum { ORC_SAMPLER_PHILOX = 0, ORC_SAMPLER_ENUMERATE = 1 };
-enum { ORC_SELECT_COUNT = 0, ORC_SELECT_ERROR = 1 };
+/* *_EARLY: "This process iterates until the maximum iterations are reached or
+ * a satisfactory model is found", reading "satisfactory" as the
+ * acceptance gate of ℓ19 (inliers / points > 0.9): the hypothesis loop stops
+ * after the first h at which the best model so far passes it (Q20). */
+enum { ORC_SELECT_COUNT = 0, ORC_SELECT_ERROR = 1, ORC_SELECT_COUNT_EARLY = 2, ORC_SELECT_ERROR_EARLY = 3 };
 
 ORC_API int orc_ransac(const float* depth, const int32_t* labels, int W, int H,
                        float fx, float fy, float cx, float cy,
@@ -471,10 +475,13 @@ ORC_API int orc_ransac(const float* depth, const int32_t* labels, int W, int H,
         if (errq_all) memcpy(errq_all + (size_t)r * n_hyp, err, (size_t)n_hyp * sizeof(uint64_t));
 
         int best = -1;                                         /* ℓ14-17 */
+        const int by_error = select_mode == ORC_SELECT_ERROR || select_mode == ORC_SELECT_ERROR_EARLY;
+        const int early = select_mode == ORC_SELECT_COUNT_EARLY || select_mode == ORC_SELECT_ERROR_EARLY;
         for (int h = 0; h < n_hyp; ++h) {
             if (cnt[h] < 0) continue;
-            if (best < 0) { best = h; continue; }
-            if (select_mode == ORC_SELECT_ERROR ? (err[h] < err[best]) : (cnt[h] > cnt[best])) best = h;
+            if (best < 0) best = h;
+            else if (by_error ? (err[h] < err[best]) : (cnt[h] > cnt[best])) best = h;
+            if (early && (int64_t)10 * cnt[best] > (int64_t)9 * n) break;   /* satisfactory */
         }
         if (best < 0) { oi[3] = ORC_DEGENERATE; continue; }
 

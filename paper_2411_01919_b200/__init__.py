@@ -30,7 +30,7 @@ _lib = ctypes.CDLL(LIB_PATH)
 
 STATUS_OK, STATUS_REJECTED, STATUS_TOO_FEW, STATUS_DEGENERATE = 0, 1, 2, 3
 SAMPLER_PHILOX, SAMPLER_ENUMERATE = 0, 1
-SELECT_COUNT, SELECT_ERROR = 0, 1
+SELECT_COUNT, SELECT_ERROR, SELECT_COUNT_EARLY, SELECT_ERROR_EARLY = 0, 1, 2, 3
 ADF_ALG1, ADF_DIVERGENCE = 0, 1
 NORMALS_GEOMETRIC, NORMALS_AS_PRINTED = 0, 1
 ENGINE_AUTO, ENGINE_TILED, ENGINE_REG, ENGINE_HOLES = 0, 1, 3, 4

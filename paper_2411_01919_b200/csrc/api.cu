@@ -99,7 +99,7 @@ pm_status ransac_impl(const float* depth, int32_t W, int32_t H, int32_t B, uint3
         errq_out = opt->errq_out;
         ev = opt->stage_events;
         if (sampler != PM_SAMPLER_PHILOX && sampler != PM_SAMPLER_ENUMERATE) return PM_ERR_INVALID_ARGUMENT;
-        if (select != PM_SELECT_COUNT && select != PM_SELECT_ERROR) return PM_ERR_INVALID_ARGUMENT;
+        if (select < PM_SELECT_COUNT || select > PM_SELECT_ERROR_EARLY) return PM_ERR_INVALID_ARGUMENT;
     }
     if (R == 0) return PM_OK;
     const size_t need = pm_ransac_workspace_bytes(W, H, R, n_hyp, B);

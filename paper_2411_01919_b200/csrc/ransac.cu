@@ -378,9 +378,10 @@ struct Best {
 PM_DEVINL void best_merge(Best& b, unsigned long long sc, int h) {
     if (sc > b.score || (sc == b.score && h < b.h)) { b.score = sc; b.h = h; }
 }
+PM_DEVINL bool select_by_error(int select) { return select == PM_SELECT_ERROR || select == PM_SELECT_ERROR_EARLY; }
 PM_DEVINL unsigned long long hyp_score(int select, int32_t c, uint64_t e) {
     if (c < 0) return 0ull;
-    return select == PM_SELECT_ERROR ? ~(unsigned long long)e : (unsigned long long)(c + 1);
+    return select_by_error(select) ? ~(unsigned long long)e : (unsigned long long)(c + 1);
 }
 // warp-cooperative: all lanes return the result
 PM_DEVINL Best warp_select(const int32_t* counts, const uint64_t* errq, int NH, int select) {
@@ -418,6 +419,45 @@ PM_DEVINL Sums sums_shfl_xor(const Sums& a, int o) {
     return b;
 }
 
+// P:292 "iterates until ... a satisfactory model is found" (the *_EARLY
+// select modes, Q20): the sequential loop of ℓ5-18 stops after the
+// first h at which the best model so far passes the acceptance gate of ℓ19.
+// Every hypothesis is scored anyway (no work to save in a batched launch);
+// the warp replays the loop's selection in chunks of 32: an inclusive
+// prefix-best scan per chunk, then the first lane whose prefix best is
+// satisfactory.  Warp-cooperative: all lanes return the result.
+PM_DEVINL int early_select(const int32_t* counts, const uint64_t* errq, int NH, int select, int n) {
+    const int lane = (int)(threadIdx.x & 31);
+    Best run{0ull, 0x7FFFFFFF};                 // best of the chunks before
+    int run_cnt = -1;
+    for (int h0 = 0; h0 < NH; h0 += 32) {
+        const int h = h0 + lane;
+        const int32_t c = h < NH ? counts[h] : -1;
+        Best b{h < NH ? hyp_score(select, c, errq[h]) : 0ull, h};
+        int bc = c;                             // count of the prefix best
+        // inclusive prefix scan of best_merge (lowest index wins ties: the
+        // sequential loop keeps the earlier model unless strictly better)
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned long long sc = __shfl_up_sync(kFull, b.score, o);
+            const int hh = __shfl_up_sync(kFull, b.h, o);
+            const int cc = __shfl_up_sync(kFull, bc, o);
+            if (lane >= o && (sc > b.score || (sc == b.score && hh < b.h))) { b.score = sc; b.h = hh; bc = cc; }
+        }
+        if (run.score > b.score || (run.score == b.score && run.h < b.h)) { b = run; bc = run_cnt; }
+        const bool ok = b.score != 0ull && (long long)10 * bc > (long long)9 * n;
+        const unsigned m = __ballot_sync(kFull, ok && h < NH);
+        if (m) {
+            const int l = __ffs(m) - 1;
+            return __shfl_sync(kFull, b.h, l);
+        }
+        run.score = __shfl_sync(kFull, b.score, 31);
+        run.h = __shfl_sync(kFull, b.h, 31);
+        run_cnt = __shfl_sync(kFull, bc, 31);
+    }
+    return run.score == 0ull ? -1 : run.h;
+}
+
 // ℓ14-17 once per region: one warp per (frame, region) -> best[f][r] (-1:
 // none / too few points).  grid = (ceil(R / 8), B).
 __global__ void __launch_bounds__(256)
@@ -428,9 +468,16 @@ ransac_select_kernel(RansacWorkspace ws, RansacArgs a) {
     const int R = ws.R, HP = ws.n_hyp_pad;
     const int32_t* off = ws.region_off + f * (size_t)(R + 1);
     int best = -1;
-    if (off[r + 1] - off[r] >= 3) {
-        const Best b = warp_select(ws.counts + (f * R + r) * HP, ws.errq + (f * R + r) * HP, ws.n_hyp, a.select);
-        best = b.score == 0ull ? -1 : b.h;
+    const int n = off[r + 1] - off[r];
+    if (n >= 3) {
+        const int32_t* cnt = ws.counts + (f * R + r) * HP;
+        const uint64_t* eq = ws.errq + (f * R + r) * HP;
+        if (a.select == PM_SELECT_COUNT_EARLY || a.select == PM_SELECT_ERROR_EARLY) {
+            best = early_select(cnt, eq, ws.n_hyp, a.select, n);
+        } else {
+            const Best b = warp_select(cnt, eq, ws.n_hyp, a.select);
+            best = b.score == 0ull ? -1 : b.h;
+        }
     }
     if ((threadIdx.x & 31) == 0) ws.best[f * R + r] = best;
 }
@@ -745,7 +792,7 @@ RansacWorkspace ransac_workspace_layout(void* base, int W, int H, int R, int n_h
 
 cudaError_t ransac_run(const RansacWorkspace& ws, const RansacArgs& a, pm_plane* planes,
                        cudaStream_t stream) {
-    const bool need_err = a.select == PM_SELECT_ERROR || a.errq_out != nullptr;
+    const bool need_err = a.select == PM_SELECT_ERROR || a.select == PM_SELECT_ERROR_EARLY || a.errq_out != nullptr;
     const int K = ws.score_K, L = ws.score_L;
     const int n_hyp_slots = ws.R * (ws.n_hyp_pad > K * L ? ws.n_hyp_pad : K * L);
     auto mark = [&](int k) {

@@ -261,6 +261,18 @@ def test_ransac_enumerate_and_select_error(pm):
     _ransac_compare(pm, d, fr["labels"].numpy(), fr["K"], 4, 64, fr["tau"], 9, select=1)
 
 
+@pytest.mark.parametrize("name,kw,H", [("C1n", {}, 64), ("C2", {}, 64), ("C2", {"holes": 0.01}, 300),
+                                       ("C1n", {}, 1)])
+def test_ransac_early_exit_selection(pm, name, kw, H):
+    """The *_EARLY select modes (P:292 early exit, Q20) against the oracle's
+    sequential loop: best_hyp, status, inliers bit-exact, refit in tolerance
+    (the warp's prefix-best scan replays the loop, chunks of 32 hypotheses)."""
+    fr = scenegen.make_config(name, **kw)
+    d, lab = fr["depth"].numpy(), fr["labels"].numpy()
+    for sel in (pm.SELECT_COUNT_EARLY, pm.SELECT_ERROR_EARLY):
+        _ransac_compare(pm, d, lab, fr["K"], 4, H, fr["tau"], 11, select=sel)
+
+
 def test_ransac_frame_ids_and_batch_invariance(pm):
     d, lab, K = scenegen.stair_stream(10, 3, W=160, H=120, n_regions=16)
     planes = pm.ransac_planes(d.to(DEV), K, lab.to(DEV), 16, 32, 0.01, 77, first_frame_id=10)

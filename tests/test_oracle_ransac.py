@@ -383,6 +383,45 @@ def test_select_modes_and_determinism():
     assert not np.array_equal(a["counts"], c["counts"])
 
 
+def test_early_exit_selection():
+    """P:292 "iterates until the maximum iterations are reached or a
+    satisfactory model is found" (Q20: satisfactory = passes the
+    0.9 gate of ℓ19; the loop stops after the first h at which the best model
+    so far does).  Pins on the oracle, from its own per-h counts / errors:
+    the early result is never later, never better-scored than the full
+    search, is accepted exactly when the full search is, equals it when no
+    prefix is satisfactory, and (COUNT) is the first h whose count passes the
+    gate -- and on these frames it does differ from the full search."""
+    differs = 0
+    for name, seed in (("C1n", 0x1919), ("C2", 5)):
+        fr = scenegen.make_config(name)
+        D, lab, K = fr["depth"].numpy(), fr["labels"].numpy(), fr["K"]
+        for full_mode, early_mode in ((oracle.SELECT_COUNT, oracle.SELECT_COUNT_EARLY),
+                                      (oracle.SELECT_ERROR, oracle.SELECT_ERROR_EARLY)):
+            a = oracle.ransac(D, lab, K, 4, 64, TAU, seed=seed, select=full_mode, debug=True)
+            e = oracle.ransac(D, lab, K, 4, 64, TAU, seed=seed, select=early_mode, debug=True)
+            assert np.array_equal(a["counts"], e["counts"]) and np.array_equal(a["errq_all"], e["errq_all"])
+            for r in range(4):
+                n = int(a["n_points"][r])
+                if a["best_hyp"][r] < 0:
+                    assert e["best_hyp"][r] == a["best_hyp"][r]
+                    continue
+                cnt, err = a["counts"][r], a["errq_all"][r]
+                hf, he = int(a["best_hyp"][r]), int(e["best_hyp"][r])
+                assert 0 <= he <= hf
+                assert (a["status"][r] == 0) == (e["status"][r] == 0)
+                if full_mode == oracle.SELECT_COUNT:
+                    assert cnt[he] <= cnt[hf]
+                    sat = np.nonzero((cnt >= 0) & (10 * cnt.astype(np.int64) > 9 * n))[0]
+                    assert he == (sat[0] if sat.size else hf)
+                else:
+                    assert err[he] >= err[hf]
+                if e["status"][r] != 0:
+                    assert he == hf and e["inliers"][r] == a["inliers"][r]
+                differs += he != hf
+    assert differs > 0
+
+
 def test_errq_is_fixed_point_sum_of_distances():
     # Q12: error = sum_i rint(min(d_i, 64) * 2^24) over ALL points (Alg. 2
     # ℓ11 sits outside the inlier test).  Compare every hypothesis' errq with
