@@ -28,6 +28,8 @@ pm.normals_from_depth(d, K)
 pm.normals_from_depth(d, K, mode=pm.NORMALS_AS_PRINTED)
 pm.ransac_planes(out, K, lab, 4, 64, 0.01, 1, debug=True)
 pm.ransac_planes(out, K, lab, 4, 300, 0.01, 1, select=pm.SELECT_ERROR, debug=True)
+pm.ransac_planes(out, K, lab, 4, 100, 0.01, 1, select=pm.SELECT_COUNT_EARLY)
+pm.ransac_planes(out, K, lab, 4, 100, 0.01, 1, select=pm.SELECT_ERROR_EARLY, debug=True)
 pm.ransac_planes(out, K, lab, 4, 1000, 0.01, 1, sampler=pm.SAMPLER_ENUMERATE, debug=True)
 ds, ls, K2 = scenegen.stair_stream(0, 3, 128, 96, 16)
 pm.process_frames(ds.cuda(), ls.cuda(), K2, 0.15, 0.03, 20, 16, 64, 0.01, 7)
