@@ -18,10 +18,13 @@
 // address at the centre cell, the strip that starts on the first image row
 // seeds N with the centre, and the last image row is peeled with S = centre.
 // Tiles whose loaded region contains an invalid depth (holes) run the same
-// walk with per-neighbour validity substitution (zero flux at holes, Q4).
+// walk with per-neighbour validity substitution (zero flux at holes, Q4), or
+// -- the FIX kernels (PM_ADF_ENGINE_HOLES, or AUTO after dropout was seen) --
+// the unchecked walk plus a recomputation of the cells next to a hole.
+// Plain passes write their rows back by cp.async.bulk copies.
 // Every path evaluates the identical _rn expression on identical operands,
-// so the result is bitwise independent of tile shape, sweeps per pass and
-// batching.
+// so the result is bitwise independent of tile shape, sweeps per pass,
+// batching and engine.
 #include <cuda_runtime.h>
 #include <float.h>
 #include <math.h>
@@ -262,9 +265,9 @@ adf_pass_kernel(const float* __restrict__ src, float* __restrict__ dst, float* _
             mbar_arrive_expect_tx(&bar, (uint32_t)(sizeof(float) * kSW * SH));
             tma_load_3d(buf0, &tmap, x0, y0, (int)frame, &bar);
         }
-        // FIX, list_mode 2: the frame flag and this tile's hole-list record
-        // fetched while the tile streams in (the record speculatively)
-        int lflag = 1;                          // the frame flag (flag_mode 2), fetched while the tile streams in
+        // fetched while the tile streams in: the frame flag (flag_mode 2) and,
+        // FIX with list_mode 2, this tile's hole-list record (speculatively)
+        int lflag = 1;
         uint4 lrec = make_uint4(0u, 0u, 0u, 0u);
         if (flag_mode == 2) lflag = frame_flags[frame];
         if (FIX && flag_mode == 2 && list_mode == 2 && threadIdx.x <= kListVecs)
