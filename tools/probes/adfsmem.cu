@@ -10,6 +10,7 @@
 //   MODE 3: MODE 0 without the per-sweep barrier (wrong; timing only)
 //   MODE 6: W / E by SHFL of the neighbour lanes' centre pair (+ one edge LDS)
 //   MODE 9: W / E by one aligned LDS.64 (wrong cells; timing only)
+//   MODE 10 (kernel kq): the quad walk, 4 columns per thread
 //   nvcc -O3 -gencode arch=compute_100a,code=sm_100a -o tools/probes/adfsmem tools/probes/adfsmem.cu
 #include <cstdint>
 #include <cstdio>
@@ -111,6 +112,91 @@ __global__ void __launch_bounds__(256, 4) k(float* out, int reps, float kc, floa
     out[blockIdx.x * 256 + threadIdx.x] = b0[threadIdx.x * 7 % (kSW * SH)];
 }
 
+// MODE 10: quad walk -- 4 columns per thread as two packed pairs, one warp
+// per 128-column row strip, 8 row parts: per row one LDS.128 (south quad),
+// scalar W (x-1) and E (x+4), one STS.128; the pairs' outer neighbours
+// (W, c2) and (c1, E) built by register moves
+template <int SH>
+__global__ void __launch_bounds__(256, 4) kq(float* out, int reps, float kc, float l2lam) {
+    extern __shared__ __align__(16) float sm[];
+    float* b0 = sm;
+    float* b1 = sm + kSW * (SH + 2);
+    for (int i = threadIdx.x; i < kSW * (SH + 2); i += 256) {
+        b0[i] = 1.0f + 1e-4f * (i & 63);
+        b1[i] = b0[i];
+    }
+    __syncthreads();
+    const P2 KC = pk(kc, kc), L2 = pk(l2lam, l2lam), M4 = pk(-4.f, -4.f);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int x = lane * 4;
+    for (int rep = 0; rep < reps; ++rep) {
+#pragma unroll 1
+        for (int t = 1; t <= T; ++t) {
+            const float* cur = (t & 1) ? b0 : b1;
+            float* nxt = (t & 1) ? b1 : b0;
+            const int ylo = t, yhi = SH - t;
+            const int q = (yhi - ylo + 7) / 8;
+            const int ys = ylo + warp * q, ye = min(ys + q, yhi);
+            if (ys < ye) {
+                const float* col = cur + x + ys * kSW;
+                float* ocol = nxt + x + ys * kSW;
+                const int offW = x == 0 ? 0 : -1, offE = x == kSW - 4 ? 3 : 4;
+                auto ld4 = [](const float* a) { return *reinterpret_cast<const float4*>(a); };
+                float4 C = ld4(col), N = ld4(col - kSW), S = ld4(col + kSW);
+                float w = col[offW], e = col[offE];
+                for (int y = ys; y < ye; ++y) {
+                    const float4 S1 = ld4(col + 2 * kSW);
+                    const float w1 = col[kSW + offW], e1 = col[kSW + offE];
+                    const P2 c01 = pk(C.x, C.y), c23 = pk(C.z, C.w);
+                    const P2 o0 = cell<0>(c01, pk(N.x, N.y), pk(S.x, S.y), pk(w, C.z), KC, L2, M4);
+                    const P2 o1 = cell<0>(c23, pk(N.z, N.w), pk(S.z, S.w), pk(C.y, e), KC, L2, M4);
+                    *reinterpret_cast<float4*>(ocol) = make_float4(plo(o0), phi(o0), plo(o1), phi(o1));
+                    N = C; C = S; S = S1; w = w1; e = e1;
+                    col += kSW; ocol += kSW;
+                }
+            }
+            __syncthreads();
+        }
+    }
+    out[blockIdx.x * 256 + threadIdx.x] = b0[threadIdx.x * 7 % (kSW * SH)];
+}
+
+template <int SH, int CPS>
+void runq(const char* name) {
+    int sms, clk;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
+    const size_t smem = sizeof(float) * 2 * kSW * (SH + 2);
+    cudaFuncSetAttribute(kq<SH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    float* o;
+    const int blocks = sms * CPS * 8;
+    cudaMalloc(&o, (size_t)blocks * 256 * 4);
+    const int reps = 50;
+    float best = 1e30f;
+    for (int r = 0; r < 3; ++r) {
+        cudaEvent_t e0, e1;
+        cudaEventCreate(&e0);
+        cudaEventCreate(&e1);
+        cudaEventRecord(e0);
+        kq<SH><<<blocks, 256, smem>>>(o, reps, -400.f, -2.7f);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float ms;
+        cudaEventElapsedTime(&ms, e0, e1);
+        if (ms < best) best = ms;
+    }
+    double per_tile = 0;
+    for (int t = 1; t <= T; ++t) per_tile += (double)(SH - 2 * t) * kSW;
+    const double cells = per_tile * reps * blocks;
+    const double cyc = best * 1e-3 * clk * 1e3;
+    cudaFuncAttributes fa;
+    cudaFuncGetAttributes(&fa, kq<SH>);
+    const double rate = cells / cyc / sms;
+    printf("%-58s regs %3d  %.3f ms  %.2f cells/clk/SM  %.1f cyc per 64 cells per SMSP\n", name, fa.numRegs, best,
+           rate, 4.0 * 64 / rate);
+    cudaFree(o);
+}
+
 template <int MODE, int SH = 52, int CPS = 4, int PD = 1>
 void run(const char* name) {
     int sms, clk;
@@ -159,6 +245,7 @@ int main() {
     run<0, 40, 5>("0, 40-row tile, 5 CTAs/SM (10 warps/SMSP)");
     run<0, 32, 6>("0, 32-row tile, 6 CTAs/SM (12 warps/SMSP)");
     run<2, 40, 5>("2, 40-row tile, 5 CTAs/SM");
+    runq<52, 4>("10 quad walk (LDS.128, 2 pairs per thread)");
     printf("%s\n", cudaGetErrorString(cudaGetLastError()));
     return 0;
 }
