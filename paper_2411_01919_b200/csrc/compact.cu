@@ -122,6 +122,47 @@ PM_DEVINL void count_lane_walk(const float* __restrict__ d, const int32_t* __res
     if (cur >= 0) atomicAdd(row + cur, cnt);
 }
 
+// The same walk with 16-byte loads: lane l takes pixels 4l..4l+3 of every
+// 128-pixel step (the histogram does not depend on the order a lane sees
+// its pixels); a quarter of the load instructions.  Needs W*H % 4 == 0 and
+// 16-byte aligned frame bases.
+constexpr int kPrefetch4 = 4;
+template <bool NEED_Z>
+PM_DEVINL void count_lane_walk4(const float* __restrict__ d, const int32_t* __restrict__ l, unsigned beg,
+                                unsigned end, int R, int lane, int* __restrict__ row) {
+    int cur = -1, cnt = 0;
+    auto take = [&](int lab, float z) {
+        const int lb = ((!NEED_Z || valid_depth(z)) && (unsigned)lab < (unsigned)R) ? lab : -1;
+        if (lb >= 0) {
+            if (lb != cur) {                           // rare: a region boundary in this lane's pixels
+                if (cur >= 0) atomicAdd(row + cur, cnt);
+                cur = lb;
+                cnt = 0;
+            }
+            ++cnt;
+        }
+    };
+    for (unsigned i00 = beg; i00 < end; i00 += 128 * kPrefetch4) {
+        int4 lr[kPrefetch4];
+        float4 zr[kPrefetch4];
+#pragma unroll
+        for (int u = 0; u < kPrefetch4; ++u) {         // all loads of kPrefetch4 steps in flight
+            const unsigned i = i00 + u * 128 + lane * 4;
+            lr[u] = i < end ? __ldg(reinterpret_cast<const int4*>(l + i)) : make_int4(-1, -1, -1, -1);
+            if (NEED_Z) zr[u] = i < end ? __ldg(reinterpret_cast<const float4*>(d + i)) : make_float4(0.f, 0.f, 0.f, 0.f);
+            else zr[u] = make_float4(1.f, 1.f, 1.f, 1.f);
+        }
+#pragma unroll
+        for (int u = 0; u < kPrefetch4; ++u) {
+            take(lr[u].x, zr[u].x);
+            take(lr[u].y, zr[u].y);
+            take(lr[u].z, zr[u].z);
+            take(lr[u].w, zr[u].w);
+        }
+    }
+    if (cur >= 0) atomicAdd(row + cur, cnt);
+}
+
 __global__ void __launch_bounds__(kWarpsPerBlock * 32)
 compact_count_lane_kernel(const float* __restrict__ depth, const int32_t* __restrict__ labels,
                           int WH, int R, int sub_tile, int n_sub, int32_t* __restrict__ hist,
@@ -138,8 +179,16 @@ compact_count_lane_kernel(const float* __restrict__ depth, const int32_t* __rest
     const unsigned end = min(beg + (unsigned)sub_tile, (unsigned)WH);
     const float* d = depth + f * WH;
     const int32_t* l = labels + f * WH;
-    if (depth_all_valid == nullptr || depth_all_valid[f] != 0) count_lane_walk<true>(d, l, beg, end, R, lane, row);
-    else count_lane_walk<false>(d, l, beg, end, R, lane, row);
+    const bool need_z = depth_all_valid == nullptr || depth_all_valid[f] != 0;
+    const bool vec = (WH & 3) == 0 && ((reinterpret_cast<uintptr_t>(depth) | reinterpret_cast<uintptr_t>(labels)) & 15) == 0;
+    if (vec) {
+        if (need_z) count_lane_walk4<true>(d, l, beg, end, R, lane, row);
+        else count_lane_walk4<false>(d, l, beg, end, R, lane, row);
+    } else if (need_z) {
+        count_lane_walk<true>(d, l, beg, end, R, lane, row);
+    } else {
+        count_lane_walk<false>(d, l, beg, end, R, lane, row);
+    }
     __syncwarp();
     int32_t* h = hist + f * (size_t)R * n_sub;
     for (int r = lane; r < R; r += 32) {
