@@ -66,6 +66,7 @@ constexpr int kHoleCap = kFixItems * kThreads / 5;
 // Per-tile record of the first pass's hole lists (list_mode 1 writes, 2
 // reads): 8 uint16 counts, then the 512-B lists -- kListVecs + 1 uint4.
 constexpr int kListVecs = kSW * 2 * 2 / 16;
+static_assert(kWarps == 8, "the hole-list record header holds 8 uint16 per-warp counts (one uint4)");
 PM_DEVINL size_t tile_index() { return ((size_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x; }
 
 struct Box { int ix0, ix1, iy0, iy1; };
