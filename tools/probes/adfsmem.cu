@@ -11,6 +11,7 @@
 //   MODE 6: W / E by SHFL of the neighbour lanes' centre pair (+ one edge LDS)
 //   MODE 9: W / E by one aligned LDS.64 (wrong cells; timing only)
 //   MODE 10 (kernel kq): the quad walk, 4 columns per thread
+//   MODE 11: odd rows take 2^x from a polynomial on the FMA pipe (fewer MUFU)
 //   nvcc -O3 -gencode arch=compute_100a,code=sm_100a -o tools/probes/adfsmem tools/probes/adfsmem.cu
 #include <cstdint>
 #include <cstdio>
@@ -29,12 +30,28 @@ __device__ __forceinline__ P2 swp(P2 a) { return pk(phi(a), plo(a)); }
 
 constexpr int kSW = 128, T = 4;
 
+// 2^x for x <= 0 on the FMA pipe (+ integer exponent add): round-to-nearest
+// range reduction by the 1.5 * 2^23 magic, degree-5 polynomial on [-0.5, 0.5]
+__device__ __forceinline__ P2 pex2_poly(P2 x) {
+    const P2 MAG = pk(12582912.0f, 12582912.0f);
+    x = pk(fmaxf(plo(x), -126.f), fmaxf(phi(x), -126.f));
+    const P2 t = padd(x, MAG);
+    const P2 f = psub(x, psub(t, MAG));
+    P2 q = pfma(f, pk(1.3333558e-3f, 1.3333558e-3f), pk(9.6181291e-3f, 9.6181291e-3f));
+    q = pfma(q, f, pk(5.5504109e-2f, 5.5504109e-2f));
+    q = pfma(q, f, pk(2.4022651e-1f, 2.4022651e-1f));
+    q = pfma(q, f, pk(6.9314718e-1f, 6.9314718e-1f));
+    q = pfma(q, f, pk(1.0f, 1.0f));
+    const int n0 = __float_as_int(plo(t)) - 0x4B400000, n1 = __float_as_int(phi(t)) - 0x4B400000;
+    return pk(__int_as_float(__float_as_int(plo(q)) + (n0 << 23)), __int_as_float(__float_as_int(phi(q)) + (n1 << 23)));
+}
+
 template <int MODE>
-__device__ __forceinline__ P2 cell(P2 C, P2 N, P2 S, P2 P, P2 KC, P2 L2, P2 M4) {
+__device__ __forceinline__ P2 cell(P2 C, P2 N, P2 S, P2 P, P2 KC, P2 L2, P2 M4, bool poly = false) {
     const P2 Cs = swp(C);
     const P2 gx = psub(Cs, P), gy = psub(S, N);
     const P2 e = pfma(pfma(gx, gx, pmul(gy, gy)), KC, L2);
-    const P2 lc = pk(ex2(plo(e)), ex2(phi(e)));
+    const P2 lc = poly ? pex2_poly(e) : pk(ex2(plo(e)), ex2(phi(e)));
     const P2 lap = pfma(M4, C, padd(padd(N, S), padd(P, Cs)));
     return pfma(lc, lap, C);
 }
@@ -89,7 +106,7 @@ __global__ void __launch_bounds__(256, 4) k(float* out, int reps, float kc, floa
                     } else {
                         P1 = pk(colW[kSW], colE[kSW]);
                     }
-                    *reinterpret_cast<P2*>(ocol) = cell<MODE>(C, N, S, Pn, KC, L2, M4);
+                    *reinterpret_cast<P2*>(ocol) = cell<MODE>(C, N, S, Pn, KC, L2, M4, MODE == 11 && (((ocol - nxt) >> 7) & 1));
                     N = C;
                     C = S;
                     S = S1;
@@ -246,6 +263,8 @@ int main() {
     run<0, 32, 6>("0, 32-row tile, 6 CTAs/SM (12 warps/SMSP)");
     run<2, 40, 5>("2, 40-row tile, 5 CTAs/SM");
     runq<52, 4>("10 quad walk (LDS.128, 2 pairs per thread)");
+    run<11>("11 odd rows: exp2 by polynomial on the FMA pipe");
+    run<0>("0 again");
     printf("%s\n", cudaGetErrorString(cudaGetLastError()));
     return 0;
 }
