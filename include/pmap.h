@@ -90,12 +90,15 @@ enum {
  * NULL, the normal image of the result (ℓ9-13, see normals_from_depth) fused
  * into the last diffusion pass.
  *   depth_in   [B][H][W] f32, read only; must not overlap depth_out.
- *   depth_out  [B][H][W] f32, written (I_smooth).
+ *   depth_out  [B][H][W] f32, written (I_smooth); 16-byte aligned (float4 /
+ *              bulk-copy rows; a tensor view at an element offset may not be:
+ *              PM_ERR_INVALID_ARGUMENT).
  *   K          host pointer; required iff normals_out != NULL.
  *   lambda     gamma of Alg. 1, 0 < lambda <= 0.25 (stability).
  *   kappa      k of Alg. 1 in metres, > 0.
  *   iters      N >= 0 (N = 0 copies depth_in).
- *   normals_out [B][3][H][W] f32 (SoA: nx plane, ny plane, nz plane) or NULL.
+ *   normals_out [B][3][H][W] f32 (SoA: nx plane, ny plane, nz plane) or NULL;
+ *              16-byte aligned like depth_out.
  *   workspace  >= pm_adf_workspace_bytes(W, H, n_frames) bytes, 256-B aligned.
  * The result is bitwise independent of n_frames and of the blocking depth. */
 PM_API pm_status pm_adf_filter(const float* depth_in, float* depth_out, int32_t W, int32_t H,

@@ -63,6 +63,9 @@ pm_status adf_impl(const float* in, float* out, int32_t W, int32_t H, int32_t B,
     if (scheme != PM_ADF_ALG1 && scheme != PM_ADF_DIVERGENCE) return PM_ERR_INVALID_ARGUMENT;
     if (nmode != PM_NORMALS_GEOMETRIC && nmode != PM_NORMALS_AS_PRINTED) return PM_ERR_INVALID_ARGUMENT;
     if (!in || !out || !dims_ok(W, H, B) || iters < 0) return PM_ERR_INVALID_ARGUMENT;
+    // the kernels write rows as float4 / bulk copies: 16-byte aligned outputs
+    if (((reinterpret_cast<uintptr_t>(out) | reinterpret_cast<uintptr_t>(normals)) & 15) != 0)
+        return PM_ERR_INVALID_ARGUMENT;
     if (!(lam > 0.0f && lam <= 0.25f) || !finite_pos(kappa)) return PM_ERR_INVALID_ARGUMENT;
     if (normals && !intrinsics_ok(K)) return PM_ERR_INVALID_ARGUMENT;
     const size_t bytes = sizeof(float) * (size_t)B * W * H;
@@ -183,6 +186,7 @@ PM_API pm_status pm_normals_from_depth_ex(const float* depth, int32_t W, int32_t
                                           pm_stream_t stream) {
     const pm::NvtxRange nvtx_("pmap:normals_from_depth");
     if (!depth || !normals_out || !dims_ok(W, H, n_frames) || !intrinsics_ok(K)) return PM_ERR_INVALID_ARGUMENT;
+    if ((reinterpret_cast<uintptr_t>(normals_out) & 15) != 0) return PM_ERR_INVALID_ARGUMENT;   // float4 rows
     if (mode != PM_NORMALS_GEOMETRIC && mode != PM_NORMALS_AS_PRINTED) return PM_ERR_INVALID_ARGUMENT;
     const size_t bytes = sizeof(float) * (size_t)n_frames * W * H;
     if (overlap(depth, bytes, normals_out, 3 * bytes)) return PM_ERR_INVALID_ARGUMENT;

@@ -858,3 +858,31 @@ def test_two_devices_in_one_process(pm):
         res.append([t.raw.cpu() if hasattr(t, "raw") else t.cpu() for t in out])
     for a, b in zip(*res):
         assert torch.equal(a, b)
+
+
+def test_auto_engine_after_dropout_and_unaligned_buffers(pm):
+    """AUTO after calls that met dropout (it then runs the hole engine) equals
+    TILED bit for bit; an output tensor 4 bytes off a 16-byte boundary is
+    rejected (the kernels write float4 / bulk-copy rows), labels 4 bytes off
+    take the scalar count walk with identical results."""
+    d, lab, K = scenegen.stair_stream(60, 4, 640, 480, 64, device=DEV)
+    for i in range(4):
+        d[i] = scenegen.dropout(d[i], 0.01, 5 + i, i)
+    ref, nref = pm.adf_filter(d, K, 0.15, 0.03, 20, engine=pm.ENGINE_TILED)
+    for _ in range(3):
+        out, nrm = pm.adf_filter(d, K, 0.15, 0.03, 20)
+        torch.cuda.synchronize()
+        assert torch.equal(out, ref) and torch.equal(nrm.nan_to_num(7.0), nref.nan_to_num(7.0))
+    big = torch.empty(d.numel() + 1, device=DEV)
+    out_u = big[1:].view(d.shape)                     # 4 bytes past a 16-byte boundary: rejected
+    with pytest.raises(pm.PMError):
+        pm.adf_filter(d, K, 0.15, 0.03, 20, out=out_u)
+    with pytest.raises(pm.PMError):
+        pm.normals_from_depth(d, K, out=torch.empty(d.numel() * 3 + 1, device=DEV)[1:].view(4, 3, 480, 640))
+    planes = pm.ransac_planes(ref, K, lab, 64, 64, 0.01, 3)
+    bl = torch.empty(lab.numel() + 1, dtype=torch.int32, device=DEV)
+    lab_u = bl[1:].view(lab.shape)
+    lab_u.copy_(lab)
+    planes_u = pm.ransac_planes(ref, K, lab_u, 64, 64, 0.01, 3)
+    torch.cuda.synchronize()
+    assert torch.equal(planes.raw, planes_u.raw)
