@@ -25,7 +25,8 @@ constexpr int kConvThreads = 256;
 __global__ void __launch_bounds__(kConvThreads)
 u16_to_metres_kernel(const uint16_t* __restrict__ mm, float* __restrict__ out, size_t n, float scale) {
     const size_t i0 = ((size_t)blockIdx.x * kConvThreads + threadIdx.x) * 4;
-    if (i0 + 3 < n && ((reinterpret_cast<uintptr_t>(mm + i0) & 7) == 0)) {
+    if (i0 + 3 < n && ((reinterpret_cast<uintptr_t>(mm + i0) & 7) == 0) &&
+        ((reinterpret_cast<uintptr_t>(out + i0) & 15) == 0)) {
         const ushort4 v = *reinterpret_cast<const ushort4*>(mm + i0);
         *reinterpret_cast<float4*>(out + i0) =
             make_float4(__fmul_rn((float)v.x, scale), __fmul_rn((float)v.y, scale), __fmul_rn((float)v.z, scale),

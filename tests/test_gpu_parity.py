@@ -886,3 +886,19 @@ def test_auto_engine_after_dropout_and_unaligned_buffers(pm):
     planes_u = pm.ransac_planes(ref, K, lab_u, 64, 64, 0.01, 3)
     torch.cuda.synchronize()
     assert torch.equal(planes.raw, planes_u.raw)
+
+
+def test_depth_u16_to_metres_any_alignment(pm):
+    """pm_depth_u16_to_metres on views at odd element offsets (input and
+    output) equals the aligned conversion: the vector path only runs where
+    both addresses allow it."""
+    mm = (torch.arange(1003, dtype=torch.int32) * 37 % 65536).to(torch.uint16).to(DEV)
+    ref = pm.depth_u16_to_metres(mm)
+    for a, b in ((1, 0), (0, 1), (3, 2)):
+        src = torch.empty(mm.numel() + a, dtype=torch.uint16, device=DEV)[a:]
+        src.copy_(mm)
+        dst = torch.empty(mm.numel() + b, device=DEV)[b:]
+        out = pm.depth_u16_to_metres(src, out=dst)
+        torch.cuda.synchronize()
+        assert torch.equal(out, ref)
+
