@@ -182,6 +182,7 @@ PM_DEVINL void sweep_pairs(const float* __restrict__ cur, float* __restrict__ nx
         ocol += kSW;
     };
     int i = 0;
+#ifndef PM_ADF_WALK_UNROLL
     for (; i + 4 <= n; i += 4) {
         step(); step(); step(); step();
     }
@@ -192,6 +193,11 @@ PM_DEVINL void sweep_pairs(const float* __restrict__ cur, float* __restrict__ nx
             if (i + 2 < n) step();
         }
     }
+#else   // A/B knob (tools/build_variant.sh): rows per unrolled step
+    constexpr int kWalkUnroll = PM_ADF_WALK_UNROLL;
+#pragma unroll(kWalkUnroll)
+    for (; i < n; ++i) step();
+#endif
     if (ye > ylast)                                 // last image row: S = C
         *reinterpret_cast<float2*>(ocol) = cellp(C, N, C, P);
 }
