@@ -369,6 +369,73 @@ ransac_score_kernel(RansacWorkspace ws, RansacArgs a) {
     }
 }
 
+// Many small regions (a chunk holding ~10+ region segments): the kernel above
+// spreads every segment over all 256 threads and pays a block reduction with
+// two barriers per segment.  Here each warp takes whole segments (regions
+// r0 + w, r0 + w + 8, ...) with its 32 / L groups of L lanes, reduces them by
+// shuffles and adds one atomic per hypothesis -- no barrier after staging.
+// The same packed evaluation and ALU-pipe count as above (bit-exact counts).
+// Used for the count-only packed layouts when the frame's average region is
+// smaller than kSmallRegionPx points (host dispatch; measured: 640x480 frames
+// with R = 1024, 300-point regions: scoring 0.43 -> 0.71 of its issue bound,
+// with R = 256, 1200-point regions, the CTA-wide kernel stays ahead).
+constexpr int kSmallRegionPx = kScoreChunk / 8;   // ~8+ segments per chunk: every warp has one
+template <int K, int L>
+__global__ void __launch_bounds__(kScoreThreads)
+ransac_score_small_kernel(RansacWorkspace ws, RansacArgs a) {
+    static_assert(K % 2 == 0 && L <= 32 && 32 % L == 0, "packed count layouts with L <= 32");
+    extern __shared__ __align__(16) float4 sp[];                 // kScoreChunk points
+    __shared__ int s_r0;
+    constexpr int GW = 32 / L;                                   // groups per warp
+    constexpr int K2 = K / 2;
+    const size_t f = blockIdx.y;
+    Chunk ck;
+    if (!stage_chunk(ws, a, f, sp, &s_r0, ck)) return;
+    const int R = ws.R, NH = ws.n_hyp;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int g = lane / L, l = lane % L;
+    const int32_t* off = ws.region_off + f * (size_t)(R + 1);
+    const float tau = a.tau;
+    for (int r = ck.r0 + w; r < R && off[r] < ck.e; r += kScoreThreads / 32) {   // warp-uniform
+        const int lo = max(ck.s, off[r]) - ck.s, hi = min(ck.e, off[r + 1]) - ck.s;
+        if (hi <= lo || off[r + 1] - off[r] < 3) continue;
+        const ulonglong2* pp = reinterpret_cast<const ulonglong2*>(ws.pairs) + (f * R + r) * (size_t)(K * L);
+        uint64_t X[K2], Y[K2], Z[K2], D[K2];
+#pragma unroll
+        for (int j = 0; j < K2; ++j) {
+            const ulonglong2 u = __ldg(pp + (j * L + l) * 2);
+            const ulonglong2 v = __ldg(pp + (j * L + l) * 2 + 1);
+            X[j] = u.x; Y[j] = u.y; Z[j] = v.x; D[j] = v.y;
+        }
+        int c[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) c[k] = 0;
+#pragma unroll 4
+        for (int i = lo + g; i < hi; i += GW) {
+            const float4 p4 = sp[i];
+            const uint64_t px = f2pk(f2s(p4.x)), py = f2pk(f2s(p4.y)), pz = f2pk(f2s(p4.z));
+#pragma unroll
+            for (int j = 0; j < K2; ++j) {
+                uint64_t d;
+                asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(X[j]), "l"(px), "l"(D[j]));
+                asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(d) : "l"(Y[j]), "l"(py));
+                asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(d) : "l"(Z[j]), "l"(pz));
+                const float2 df = f2up(d);
+                count_lt(c[2 * j], fabsf(df.x), tau);
+                count_lt(c[2 * j + 1], fabsf(df.y), tau);
+            }
+        }
+        int32_t* counts = ws.counts + (f * R + r) * ws.n_hyp_pad;
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+#pragma unroll
+            for (int o = L; o < 32; o <<= 1) c[k] += __shfl_xor_sync(kFull, c[k], o);
+            const int h = l + k * L;                 // pair j holds k = 2j, 2j + 1 (the hyp kernel's layout)
+            if (g == 0 && h < NH && c[k] > 0) atomicAdd(counts + h, c[k]);
+        }
+    }
+}
+
 // ---- ℓ14-17 selection: argmax count (or argmin error), ties -> lowest h.
 // Every caller evaluates the same order-free rule, so results agree.
 struct Best {
@@ -749,6 +816,12 @@ cudaError_t ransac_setup_attributes() {
     PM_ATTR(1, 8) PM_ATTR(2, 8) PM_ATTR(4, 8) PM_ATTR(8, 8) PM_ATTR(8, 16) PM_ATTR(8, 32)
     PM_ATTR(8, 64) PM_ATTR(8, 128) PM_ATTR(8, 256) PM_ATTR(16, 256)
 #undef PM_ATTR
+#define PM_ATTR_SMALL(KK, LL)                                                                              \
+    if (e == cudaSuccess)                                                                                  \
+        e = cudaFuncSetAttribute((const void*)ransac_score_small_kernel<KK, LL>,                           \
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(sizeof(float4) * kScoreChunk));
+    PM_ATTR_SMALL(2, 8) PM_ATTR_SMALL(4, 8) PM_ATTR_SMALL(8, 8) PM_ATTR_SMALL(8, 16) PM_ATTR_SMALL(8, 32)
+#undef PM_ATTR_SMALL
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute((const void*)ransac_refit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)kRefitSmem);
@@ -802,8 +875,17 @@ cudaError_t ransac_run(const RansacWorkspace& ws, const RansacArgs& a, pm_plane*
     mark(0);
     const dim3 g_score((unsigned)(((size_t)ws.W * ws.H + kScoreChunk - 1) / kScoreChunk), ws.B);
     bool launched = false;
+    // many small regions: the warp-per-segment kernel (count-only packed layouts)
+    const bool small = !need_err && (size_t)ws.W * ws.H < (size_t)kSmallRegionPx * (size_t)ws.R;
+#define PM_SCORE_SMALL(KK, LL)                                                                             \
+    if (!launched && small && K == KK && L == LL) {                                                        \
+        ransac_score_small_kernel<KK, LL><<<g_score, kScoreThreads, sizeof(float4) * kScoreChunk, stream>>>(ws, a); \
+        launched = true;                                                                                   \
+    }
+    PM_SCORE_SMALL(2, 8) PM_SCORE_SMALL(4, 8) PM_SCORE_SMALL(8, 8) PM_SCORE_SMALL(8, 16) PM_SCORE_SMALL(8, 32)
+#undef PM_SCORE_SMALL
 #define PM_SCORE(KK, LL)                                                                                   \
-    if (K == KK && L == LL) {                                                                              \
+    if (!launched && K == KK && L == LL) {                                                                 \
         if (need_err)                                                                                      \
             ransac_score_kernel<KK, LL, true>                                                              \
                 <<<g_score, kScoreThreads, score_smem_bytes<KK, LL, true>(), stream>>>(ws, a);             \

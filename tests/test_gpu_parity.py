@@ -902,3 +902,27 @@ def test_depth_u16_to_metres_any_alignment(pm):
         torch.cuda.synchronize()
         assert torch.equal(out, ref)
 
+
+
+@pytest.mark.parametrize("H", [16, 64, 200])
+def test_ransac_small_region_kernel(pm, H):
+    """Frames whose regions average fewer than 512 points score with the
+    warp-per-segment kernel (count-only runs: no per-hypothesis error
+    requested): per-hypothesis counts, winners, status and inliers bit-exact
+    vs the oracle, refit within tolerance."""
+    fr = scenegen.make_config("C2", W=320, H=240)
+    d = fr["depth"].numpy()
+    v, u = np.mgrid[0:240, 0:320]
+    lab = ((v // 8) * 40 + u // 8).astype(np.int32)          # 1200 regions of 64 px
+    lab[(lab % 17) == 4] = -1
+    R = 1200
+    planes, counts, _ = pm.ransac_planes(torch.from_numpy(d).to(DEV), fr["K"], torch.from_numpy(lab).to(DEV), R, H,
+                                         fr["tau"], 21, debug="counts")
+    torch.cuda.synchronize()
+    ref = oracle.ransac(d, lab, fr["K"], R, H, fr["tau"], 21, debug=True)
+    assert np.array_equal(counts.cpu().numpy(), ref["counts"])
+    assert np.array_equal(planes.best_hyp.cpu().numpy(), ref["best_hyp"])
+    assert np.array_equal(planes.status.cpu().numpy(), ref["status"])
+    assert np.array_equal(planes.inliers.cpu().numpy(), ref["inliers"])
+    ok = ref["status"] <= 1
+    assert np.abs(planes.n.cpu().numpy()[ok] - ref["n"][ok]).max() <= REFIT_TOL
