@@ -412,6 +412,7 @@ ransac_score_small_kernel(RansacWorkspace ws, RansacArgs a) {
         for (int k = 0; k < K; ++k) c[k] = 0;
 #pragma unroll 4
         for (int i = lo + g; i < hi; i += GW) {
+            PM_CHECK(i >= 0 && i < kScoreChunk);
             const float4 p4 = sp[i];
             const uint64_t px = f2pk(f2s(p4.x)), py = f2pk(f2s(p4.y)), pz = f2pk(f2s(p4.z));
 #pragma unroll

@@ -44,6 +44,10 @@ labels, nreg, _ = pm.segment_regions(n2, 30, 90, 100, 64, edges=True)
 polys = pm.region_polygons(labels, 64)
 pm.rasterize_polygons(polys, 256, 160)
 pl = pm.ransac_planes(d2, fr2["K"], labels, 64, 64, 0.01, 3)
+# many small regions: the warp-per-segment scoring kernel (count-only)
+v, u = torch.meshgrid(torch.arange(160, device="cuda"), torch.arange(256, device="cuda"), indexing="ij")
+grid = ((v // 8) * 32 + u // 8).to(torch.int32)
+pm.ransac_planes(d2, fr2["K"], grid, 640, 64, 0.01, 3, debug="counts")
 pm.lift_polygon_vertices(polys, pl, fr2["K"])
 torch.cuda.synchronize()
 print("sanitize run ok")
